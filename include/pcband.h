@@ -1,0 +1,215 @@
+/*
+ * pcband.h — C ABI of the B200-native compensated-Yee band solver (libpcband.so).
+ *
+ * Method: Jin & Xie, arXiv 2511.17107 ("PAPER.md" below; "P:123" = PAPER.md line 123).
+ * The library computes, matrix-free on one GPU, in complex FP64,
+ *
+ *     Op(k) = A_c M_eps A_c^H + gamma(k) B^H B                     (display:kc_formulation)
+ *
+ * on an N^3 Bloch-shifted Yee grid, its FFT-diagonal preconditioner K_P^{-1}, and the
+ * smallest eigenvalues omega^2 of Op(k) by block LOBPCG with soft locking.
+ *
+ * Conventions (all entry points)
+ * ------------------------------
+ *  - Complex numbers are interleaved (re, im) doubles (== cuDoubleComplex == torch.complex128).
+ *  - A field is 3*N^3 complex values, component-major [c][z][y][x], x fastest (the Kronecker
+ *    factor of axis 1 is the last one).  A block of ncols fields is column-major: column j starts at
+ *    base + j*ld (ld in complex elements, ld >= 3*N^3).
+ *  - Fourier coordinates: x = F3^H H, F_ij = w^{(i-1)(j-1)}/sqrt(N), w = exp(+2 pi i/N)
+ *    (P:274), i.e. x = numpy.fft.fftn(H, norm="ortho") per component, modes m unshifted, same
+ *    [c][m3][m2][m1] layout.
+ *  - Device pointers (X, Y, R, P, evecs) are caller-owned CUDA device memory on the context's
+ *    device; they must not alias each other.  Host pointers are noted as such.
+ *  - stream arguments are cudaStream_t passed as void* (NULL = legacy default stream).  pc_apply /
+ *    pc_precond / pc_apply_eps / pc_fft3 are asynchronous and stream-ordered; pc_bands is synchronous.
+ *  - Calls on one context must be serialised by the caller (the workspace is per context).
+ *    Different contexts share nothing and may be used concurrently.
+ *
+ * Errors: every int-returning call returns PC_OK (0) on success, a negative PC_E* code on failure
+ * (no output written; message via pc_last_error(), thread-local), or PC_ENOTCONV (1) from pc_bands
+ * when at least one k-point hit maxit (its best pairs are still returned, status[k] = 1;
+ * SPEC "max_iter exceeded -> converged=false and best available pairs").
+ */
+#ifndef PCBAND_H
+#define PCBAND_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct pc_ctx pc_ctx; /* opaque, library-owned */
+
+enum {
+  PC_OK = 0,
+  PC_ENOTCONV = 1,  /* pc_bands: some k-point did not reach tol within maxit                       */
+  PC_EINVAL = -1,   /* bad argument: unsupported N, non-Hermitian eps1, singular A, bad sizes ...    */
+  PC_ENOTPD = -2,   /* eps1 is not positive definite (P:69 requires HPD)                             */
+  PC_ECUDA = -3,    /* a CUDA runtime error (message has the CUDA string)                            */
+  PC_ENOMEM = -4,   /* device allocation failed                                                      */
+  PC_ENUMERIC = -5  /* pc_bands: Rayleigh-Ritz breakdown that restarting could not repair            */
+};
+
+/* Discretisation of eps^{-1} (Section 3 of the paper). */
+enum {
+  PC_EPS_DIAGONAL = 0, /* M_ii = (eps_ii - 1) I_i + I, off-diagonal blocks 0      */
+  PC_EPS_CROSSDOF = 1, /* off-diagonal eps_ij S_ij, S_ij = (I_i T_ij + T_ij I_j)/2      */
+  PC_EPS_TRIVIAL = 2   /* off-diagonal eps_ij I_V (pointwise volume indicator)          */
+};
+
+enum { PC_SPACE_FOURIER = 0, PC_SPACE_REAL = 1 };
+enum { PC_FFT_TO_FOURIER = 0 /* x = F3^H H */, PC_FFT_TO_REAL = 1 /* H = F3 x */ };
+
+/* hpd_flags bits reported by pc_info (Assumptions 1-3; Props). */
+enum {
+  PC_HPD_ASSUMP1 = 1,    /* spec(eps1) in (0, 1]                      */
+  PC_HPD_SDD = 2,        /* eps1 strictly diagonally dominant          */
+  PC_HPD_ZERO_OFFD = 4,  /* at least one off-diagonal entry is zero    */
+  PC_HPD_GUARANTEED = 8  /* Assump.1 and (SDD or zero off-diagonal): M_CrossDoF / M_Trivial HPD */
+};
+
+/*
+ * pc_create — build a context for one (lattice, grid, eps1, geometry) problem.
+ *   A[9]       host, row-major 3x3 whose COLUMNS are a_1, a_2, a_3: A[3*r+c] = (a_c)_r.
+ *              Must be invertible; B = A^{-1} enters the shifted blocks (reading R3:
+ *              Dhat_i = sum_j b_ji D_{1,j} + i k_i D_{0,i}).
+ *   n          grid division N (h = 1/N), one of the sizes listed by pc_supported_n().
+ *   eps1[18]   host, 3x3 complex row-major interleaved (re,im): the inverse permittivity inside
+ *              Omega_1.  Must be Hermitian (|e_ij - conj e_ji| <= 1e-14 max|e|) -> else
+ *              PC_EINVAL, and positive definite -> else PC_ENOTPD.  Violations of Assumptions 1-3
+ *              only set pc_info flags ("hpd_report never blocks a run", SPEC).
+ *   masks      host, uint8, 4*N^3: I_1, I_2, I_3, I_V, each [z][y][x], entries 0/1,
+ *              sampled at the DoF locations (reading R6).  Copied to the device; not retained.
+ *   eps_mode   PC_EPS_*.  PC_EPS_DIAGONAL with non-zero off-diagonal eps1 -> PC_EINVAL.
+ *   gamma_override  > 0: use this penalty for every k; <= 0: the practical rule P:457-462.
+ *   device     CUDA device ordinal.
+ * On success *out receives the context (free with pc_destroy).
+ */
+int pc_create(pc_ctx **out, const double A[9], int n, const double eps1[18], const uint8_t *masks,
+              int eps_mode, double gamma_override, int device);
+
+/*
+ * pc_apply — Y = Op(k) X for ncols columns (P:523-529 / display:matrixfree_finalform).
+ *   space = PC_SPACE_FOURIER: X, Y are Fourier-coordinate fields; Y = K_A F3^H M F3 K_A^H X
+ *           + gamma K_B X, computed as one inverse and one forward 3-D DFT per column with the
+ *           curl symbol fused into the first pass and K_A + gamma K_B into the last.
+ *   space = PC_SPACE_REAL: X, Y are real-space face fields H; Y = (A_c M A_c^H + gamma B^H B) X.
+ *   k[3]  host, Bloch vector (Cartesian).  X, Y device, ld >= 3N^3, ncols >= 0
+ *   (ncols = 0 is a no-op).  X and Y must not alias.
+ */
+int pc_apply(pc_ctx *ctx, const double k[3], const void *X, void *Y, int ncols, long long ld,
+             int space, void *stream);
+
+/*
+ * pc_precond — P = K_P^{-1} R per Fourier mode, K_P = K_A K_A^H + gamma K_B
+ * = |kappa|^2 I + (gamma - 1) conj(kappa) kappa^T, closed form
+ * P = R/|kappa|^2 - (gamma-1)/(gamma |kappa|^4) conj(kappa)(kappa^T R); modes with
+ * |kappa|^2 <= 1e-28 max|kappa|^2 pass through unchanged (reading R7).  Fourier coordinates only.
+ * R, P device; P may equal R (in place).
+ */
+int pc_precond(pc_ctx *ctx, const double k[3], const void *R, void *P, int ncols, long long ld,
+               void *stream);
+
+/*
+ * pc_apply_eps — debug/parity entry: Y = M_eps E in real space, E edge fields.
+ */
+int pc_apply_eps(pc_ctx *ctx, const void *E, void *Y, int ncols, long long ld, void *stream);
+
+/*
+ * pc_fft3 — debug/parity entry: unitary 3-D DFT of each component.
+ *   direction PC_FFT_TO_FOURIER: Y = F3^H X (numpy fftn, ortho); PC_FFT_TO_REAL: Y = F3 X.
+ *   Y may equal X (in place).
+ */
+int pc_fft3(pc_ctx *ctx, const void *X, void *Y, int ncols, long long ld, int direction,
+            void *stream);
+
+/*
+ * pc_bands — the nev smallest eigenvalues omega^2 of Op(k) at each of nk Bloch vectors
+ * (kernel-compensation formulation P:254-262; LOBPCG with soft locking P:1055-1056).
+ *   kpts     host, nk*3 Cartesian Bloch vectors.
+ *   nev      number of eigenvalues (>= 1); block size = nev + guard (pc_set_option "guard",
+ *            default 5, reading R14).
+ *   tol      convergence when Res_j = ||Op x_j - w_j x_j|| / ||x_j|| <= tol for all j < nev
+ *            (the paper uses 1e-5).
+ *   maxit    iteration cap (SPEC default 500).
+ *   seed     start block of k-point i is drawn from a counter-based generator keyed by
+ *            (seed, i) — independent of how k-points are split across GPUs.
+ *   omega2   host out, nk*nev, ascending per k.  At k = 0 exactly the 3-dimensional null space
+ *            (constant fields) is deflated and the nev smallest positive eigenvalues
+ *            are returned (reading R12).
+ *   resid    host out (may be NULL), nk*nev final Res_j.
+ *   iters    host out (may be NULL), nk iteration counts.
+ *   status   host out (may be NULL), nk: 0 converged, 1 maxit reached.
+ *   evecs    NULL, or device buffer of nk*nev columns (ld = 3N^3), k-major: Fourier-coordinate
+ *            eigenvectors, unit 2-norm.
+ * Returns PC_OK, PC_ENOTCONV, or a negative error.
+ */
+int pc_bands(pc_ctx *ctx, const double *kpts, int nk, int nev, double tol, int maxit,
+             unsigned long long seed, double *omega2, double *resid, int *iters, int *status,
+             void *evecs);
+
+/* Penalty gamma used for k (override if set, else P:457-462). */
+double pc_gamma(const pc_ctx *ctx, const double k[3]);
+
+/* hpd_flags: PC_HPD_* bits for eps1; ws_bytes_per_col: apply workspace bytes per column. */
+int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
+
+/*
+ * pc_set_option — tuning knobs (return PC_EINVAL for unknown keys):
+ *   "guard"        extra LOBPCG block columns beyond nev (default 5)
+ *   "apply_chunk"  max columns per batched apply (default 0 = all at once)
+ *   "profile"      1: time every kernel class with CUDA events (read with pc_stats), 0: off
+ *   "drop_tol"     Rayleigh-Ritz rank threshold on the scaled Gram eigenvalues (default 1e-12)
+ *   "kindex_offset" global index of kpts[0] in pc_bands (start-block seeds are keyed by it, so
+ *                  results do not depend on how a k-path is split across GPUs; default 0)
+ */
+int pc_set_option(pc_ctx *ctx, const char *key, double value);
+
+/*
+ * pc_stats — cumulative per-kernel-class launch counts and CUDA-event durations (ms) since the
+ * last reset, recorded when option "profile" = 1.  out: host, 2*PC_NSTAT doubles laid out
+ * [count_0, ms_0, count_1, ms_1, ...] in the order of enum pc_stat.  reset != 0 clears them.
+ */
+enum {
+  PC_STAT_FFT_Z_KAH = 0,   /* first inverse pass with K_A^H fused      */
+  PC_STAT_FFT_MID = 1,     /* plain pencil passes                       */
+  PC_STAT_EPS = 2,         /* real-space M_eps stencil                  */
+  PC_STAT_FFT_Z_KA = 3,    /* last forward pass with K_A + gamma K_B    */
+  PC_STAT_RESID = 4,       /* residual + K_P^{-1} + norms               */
+  PC_STAT_GRAM = 5,        /* S^H [S AS] Gram products                  */
+  PC_STAT_RR = 6,          /* on-device Rayleigh-Ritz                   */
+  PC_STAT_UPDATE = 7,      /* block updates X, P, AX, AP                */
+  PC_STAT_OTHER = 8,       /* init, reductions, copies                  */
+  PC_NSTAT = 9
+};
+int pc_stats(pc_ctx *ctx, double *out, int reset);
+
+/*
+ * pc_debug_heevj — test entry for the on-device Jacobi eigensolver used by the Rayleigh-Ritz step:
+ * A_host (n x n complex, column-major, Hermitian, 1 <= n <= 80) -> w_host ascending eigenvalues,
+ * V_host (may be NULL) eigenvectors (column-major), *sweeps Jacobi sweeps used.  Synchronous,
+ * current device.
+ */
+int pc_debug_heevj(const double *A_host, int n, double *w_host, double *V_host, int *sweeps);
+
+/*
+ * pc_debug_pass — test entry: one pencil pass of the pc_apply pipeline on ncols columns (device,
+ * ld).  kind 0: plain unnormalised 1-D DFT along axis (0 x, 1 y, 2 z), sign dir (-1: e^{-},
+ * +1: e^{+}), output scaled by scale; kind 1: u = scale * K_A^H X then e^{+} DFT along z;
+ * kind 2: e^{-} DFT along z of X then K_A (.) + gamma K_B XH.  Synchronous.
+ */
+int pc_debug_pass(pc_ctx *ctx, const double k[3], int kind, int axis, int dir, const void *X, void *Y,
+                  const void *XH, int ncols, long long ld, double scale);
+
+/* Supported grid sizes: writes up to cap values into sizes, returns how many exist. */
+int pc_supported_n(int *sizes, int cap);
+
+void pc_destroy(pc_ctx *ctx);
+const char *pc_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* PCBAND_H */

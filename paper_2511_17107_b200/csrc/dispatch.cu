@@ -1,0 +1,34 @@
+// Runtime dispatch of FFT passes over the compiled grid sizes.
+#include "kernels.h"
+#include "fft_sizes.h"
+
+#define PC_DECL(N)                                                                                        \
+  cudaError_t fft_launch_##N(int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,       \
+                             const ColPtrs& xh, int ncols, const PassArgsH& a, cudaStream_t st);
+PC_FFT_SIZES(PC_DECL)
+#undef PC_DECL
+
+int fft_supported(int n) {
+#define PC_CASE(N) if (n == N) return 1;
+  PC_FFT_SIZES(PC_CASE)
+#undef PC_CASE
+  return 0;
+}
+
+int fft_supported_list(int* sizes, int cap) {
+  int cnt = 0;
+#define PC_ADD(N) { if (sizes && cnt < cap) sizes[cnt] = N; cnt++; }
+  PC_FFT_SIZES(PC_ADD)
+#undef PC_ADD
+  return cnt;
+}
+
+cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
+                            const ColPtrs& xh, int ncols, const PassArgsH& a, cudaStream_t st) {
+  switch (n) {
+#define PC_SW(N) case N: return fft_launch_##N(axis, dir, kind, in, out, xh, ncols, a, st);
+    PC_FFT_SIZES(PC_SW)
+#undef PC_SW
+    default: return cudaErrorInvalidValue;
+  }
+}

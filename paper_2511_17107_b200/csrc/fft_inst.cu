@@ -1,0 +1,40 @@
+// Instantiation of the FFT pass kernels for one grid size N (compiled once per N with
+// -DPC_FFT_N=<N>, see Makefile) -- keeps the per-file compile time small and parallel.
+#include "fft_pass.cuh"
+
+#ifndef PC_FFT_N
+#error "compile with -DPC_FFT_N=<N>"
+#endif
+#define PC_CAT2(a, b) a##b
+#define PC_CAT(a, b) PC_CAT2(a, b)
+
+template <int AXIS, int DIR, int OP, int C>
+static cudaError_t run_one(const ColPtrs& in, const MutColPtrs& out, const ColPtrs& xh, int ncols,
+                           const PassArgs& a, cudaStream_t st) {
+  constexpr int N = PC_FFT_N;
+  using Cfg = TileCfg<N, C>;
+  auto kern = fft_pass_kernel<N, AXIS, DIR, OP, C>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid((N / Cfg::TP) * N, C == 3 ? ncols : 3 * ncols);
+  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, xh, a);
+  return cudaGetLastError();
+}
+
+cudaError_t PC_CAT(fft_launch_, PC_FFT_N)(int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
+                                          const ColPtrs& xh, int ncols, const PassArgs& a, cudaStream_t st) {
+  if (kind == 1) return run_one<2, +1, OP_KAH, 3>(in, out, xh, ncols, a, st);
+  if (kind == 2) return run_one<2, -1, OP_KAG, 3>(in, out, xh, ncols, a, st);
+  if (dir < 0) {
+    if (axis == 0) return run_one<0, -1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+    if (axis == 1) return run_one<1, -1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+    return run_one<2, -1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+  }
+  if (axis == 0) return run_one<0, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+  if (axis == 1) return run_one<1, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+  return run_one<2, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+}

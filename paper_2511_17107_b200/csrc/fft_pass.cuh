@@ -1,0 +1,222 @@
+// One pencil pass of the batched 3-component 3-D FFT (complex FP64), with the operator's
+// Fourier-symbol work fused into the first / last pass of pc_apply.
+//
+// A CTA owns a tile of TP pencils of length N along AXIS (0 = x, 1 = y, 2 = z) for C components
+// (C = 3 when the fused symbol op needs all field components of a mode).  The tile is staged
+// HBM -> shared memory with cp.async (16 B per complex, coalesced: TP consecutive x for the y/z
+// passes, TP whole rows for the x pass), transformed in shared memory by a two-step Stockham
+// split N = R1 * R2 (register codelets + one twiddle stage), and written back coalesced.
+//
+// Shared layout: s[(c*N + j)*TPP + p], TPP = TP + 1 (odd pitch: conflict-free 16-B accesses
+// both for p-fastest and j-fastest thread mappings).
+//
+// OP_KAH   (prologue): u = scale * (xhat x conj(kappa))   = K_A^H xhat
+// OP_KAG   (epilogue): y = kappa x s + gamma conj(kappa) (kappa . xhat)
+// with kappa_i(m) = sum_a ktab[(3 i + a) N + m_a]  (Dhat_i symbols, reading R3).
+#pragma once
+#include "kernels.h"
+#include "dft.cuh"
+
+enum { OP_NONE = 0, OP_KAH = 1, OP_KAG = 2 };
+
+template <int N>
+struct FftPlan;
+// R1 >= R2 preferred: the thread count is TP * R1.
+#define PC_PLAN(N_, R1_, R2_) \
+  template <>                 \
+  struct FftPlan<N_> {        \
+    static constexpr int R1 = R1_, R2 = R2_; \
+  };
+PC_PLAN(4, 2, 2)
+PC_PLAN(6, 3, 2)
+PC_PLAN(8, 4, 2)
+PC_PLAN(10, 5, 2)
+PC_PLAN(12, 4, 3)
+PC_PLAN(16, 4, 4)
+PC_PLAN(20, 5, 4)
+PC_PLAN(24, 6, 4)
+PC_PLAN(32, 8, 4)
+PC_PLAN(40, 8, 5)
+PC_PLAN(48, 8, 6)
+PC_PLAN(64, 8, 8)
+PC_PLAN(80, 10, 8)
+PC_PLAN(96, 12, 8)
+PC_PLAN(100, 10, 10)
+PC_PLAN(120, 15, 8)
+PC_PLAN(128, 16, 8)
+PC_PLAN(160, 16, 10)
+PC_PLAN(192, 16, 12)
+PC_PLAN(240, 16, 15)
+PC_PLAN(256, 16, 16)
+#undef PC_PLAN
+
+// largest power of two dividing n, capped
+constexpr int pow2_div(int n, int cap) {
+  int t = 1;
+  while (t < cap && n % (2 * t) == 0) t *= 2;
+  return t;
+}
+template <int N, int C>
+struct TileCfg {
+  static constexpr int TP = pow2_div(N, C == 3 ? 8 : 16);
+  static constexpr int TPP = TP + 1;
+  static constexpr int NT = TP * FftPlan<N>::R1;
+  static constexpr size_t SMEM = (size_t)C * N * TPP * sizeof(cplx) + (size_t)N * sizeof(cplx);
+};
+
+// PassArgs: tw[j] = exp(-2 pi i j/N); ktab = [3 comps][3 axes][N] symbol pieces (OP_KAH/OP_KAG);
+// gamma (OP_KAG); scale (OP_KAH: folded 1/N^3; OP_NONE: applied at store if != 1).
+typedef PassArgsH PassArgs;
+
+template <int N>
+DEV cplx kappa_i(const cplx* kt, int i, int m1, int m2, int m3) {
+  const cplx* b = kt + 3 * i * N;
+  return ldg(b + m1) + ldg(b + N + m2) + ldg(b + 2 * N + m3);
+}
+
+// Tile geometry: element (c, j, p) of tile t -> offset within one column, and its mode triple.
+template <int N, int AXIS, int TP>
+struct TileMap {
+  int base;   // offset of (j=0, p=0)
+  int sj, sp; // strides of j and p
+  int fixed_a, fixed_b;
+  DEV TileMap(int t) {
+    constexpr int NT_ = N / TP;
+    int q = t / NT_, r = (t % NT_) * TP;
+    if (AXIS == 2) {        // pencils along z, tile = TP consecutive x at fixed y = q
+      base = q * N + r; sj = N * N; sp = 1; fixed_a = q; fixed_b = r;
+    } else if (AXIS == 1) { // pencils along y, tile = TP consecutive x at fixed z = q
+      base = q * N * N + r; sj = N; sp = 1; fixed_a = q; fixed_b = r;
+    } else {                // pencils along x, tile = TP consecutive rows y at fixed z = q
+      base = q * N * N + r * N; sj = 1; sp = N; fixed_a = q; fixed_b = r;
+    }
+  }
+  DEV int off(int j, int p) const { return base + j * sj + p * sp; }
+  // mode indices (m1 = x, m2 = y, m3 = z) of element (j, p)
+  DEV void modes(int j, int p, int& m1, int& m2, int& m3) const {
+    if (AXIS == 2) { m3 = j; m2 = fixed_a; m1 = fixed_b + p; }
+    else if (AXIS == 1) { m2 = j; m3 = fixed_a; m1 = fixed_b + p; }
+    else { m1 = j; m3 = fixed_a; m2 = fixed_b + p; }
+  }
+};
+
+template <int N, int AXIS, int DIR, int OP, int C>
+__global__ void __launch_bounds__(TileCfg<N, C>::NT)
+fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a) {
+  constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
+  static_assert(R1 * R2 == N, "bad plan");
+  constexpr int TP = TileCfg<N, C>::TP, TPP = TileCfg<N, C>::TPP, NT = TileCfg<N, C>::NT;
+  constexpr int N3 = N * N * N;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  cplx* s = reinterpret_cast<cplx*>(smem_raw);
+  cplx* tw = s + C * N * TPP;
+
+  const int tid = threadIdx.x;
+  const TileMap<N, AXIS, TP> tm(blockIdx.x);
+  int col, comp0;
+  if (C == 3) { col = blockIdx.y; comp0 = 0; }
+  else { col = blockIdx.y / 3; comp0 = blockIdx.y % 3; }
+  const cplx* gin = in.p[col] + (long long)comp0 * N3;
+  cplx* gout = out.p[col] + (long long)comp0 * N3;
+
+  // ---- stage tile into shared memory
+  for (int e = tid; e < C * N * TP; e += NT) {
+    int c, j, p;
+    if (AXIS == 0) { j = e % N; p = (e / N) % TP; c = e / (N * TP); }
+    else { p = e % TP; j = (e / TP) % N; c = e / (TP * N); }
+    cp_async16(&s[(c * N + j) * TPP + p], gin + (long long)c * N3 + tm.off(j, p));
+  }
+  cp_async_commit();
+  for (int j = tid; j < N; j += NT) tw[j] = ldg(a.tw + j);
+  cp_async_wait<0>();
+  __syncthreads();
+
+  // ---- prologue: u = scale * (xhat x conj(kappa))
+  if constexpr (OP == OP_KAH) {
+    for (int e = tid; e < N * TP; e += NT) {
+      int p = e % TP, j = e / TP;
+      int m1, m2, m3;
+      tm.modes(j, p, m1, m2, m3);
+      cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
+      cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
+      cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
+      cplx x1 = s[(0 * N + j) * TPP + p], x2 = s[(1 * N + j) * TPP + p], x3 = s[(2 * N + j) * TPP + p];
+      // (x x conj k)_1 = x2 ck3 - x3 ck2, _2 = x3 ck1 - x1 ck3, _3 = x1 ck2 - x2 ck1
+      cplx u1 = cmul(x2, conjg(k3)) - cmul(x3, conjg(k2));
+      cplx u2 = cmul(x3, conjg(k1)) - cmul(x1, conjg(k3));
+      cplx u3 = cmul(x1, conjg(k2)) - cmul(x2, conjg(k1));
+      s[(0 * N + j) * TPP + p] = a.scale * u1;
+      s[(1 * N + j) * TPP + p] = a.scale * u2;
+      s[(2 * N + j) * TPP + p] = a.scale * u3;
+    }
+    __syncthreads();
+  }
+
+  // ---- step A: R2 DFTs of size R1 (stride R2) + twiddle W_N^{j2 k1}; in place
+  for (int it = tid; it < C * TP * R2; it += NT) {
+    int p = it % TP, j2 = (it / TP) % R2, c = it / (TP * R2);
+    cplx v[R1];
+#pragma unroll
+    for (int j1 = 0; j1 < R1; j1++) v[j1] = s[(c * N + j2 + R2 * j1) * TPP + p];
+    Dft<R1, DIR>::run(v);
+#pragma unroll
+    for (int k1 = 0; k1 < R1; k1++) {
+      cplx w = tw[(j2 * k1) % N];
+      if (DIR > 0) w.y = -w.y;
+      s[(c * N + j2 + R2 * k1) * TPP + p] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+    }
+  }
+  __syncthreads();
+
+  // ---- step B: R1 DFTs of size R2 (contiguous blocks) -> natural order k1 + R1 k2
+  {
+    const int p = tid % TP, k1 = tid / TP;  // NT = TP * R1: one item per thread per component
+#pragma unroll 1
+    for (int c = 0; c < C; c++) {
+      cplx v[R2];
+#pragma unroll
+      for (int j2 = 0; j2 < R2; j2++) v[j2] = s[(c * N + R2 * k1 + j2) * TPP + p];
+      Dft<R2, DIR>::run(v);
+      __syncthreads();
+#pragma unroll
+      for (int k2 = 0; k2 < R2; k2++) s[(c * N + k1 + R1 * k2) * TPP + p] = v[k2];
+    }
+  }
+  __syncthreads();
+
+  // ---- store (with fused epilogue)
+  if constexpr (OP == OP_KAG) {
+    const cplx* gx = xh.p[col];
+    for (int e = tid; e < N * TP; e += NT) {
+      int j, p;
+      if (AXIS == 0) { j = e % N; p = e / N; } else { p = e % TP; j = e / TP; }
+      int m1, m2, m3;
+      tm.modes(j, p, m1, m2, m3);
+      cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
+      cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
+      cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
+      int o = tm.off(j, p);
+      cplx x1 = ldg(gx + o), x2 = ldg(gx + N3 + o), x3 = ldg(gx + 2 * N3 + o);
+      cplx s1 = s[(0 * N + j) * TPP + p], s2 = s[(1 * N + j) * TPP + p], s3 = s[(2 * N + j) * TPP + p];
+      // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T)
+      cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
+      kx = a.gamma * kx;
+      cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), kx);
+      cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), kx);
+      cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), kx);
+      gout[o] = y1;
+      gout[N3 + o] = y2;
+      gout[2 * N3 + o] = y3;
+    }
+  } else {
+    const double sc = (OP == OP_NONE) ? a.scale : 1.0;  // OP_KAH applied it in the prologue
+    for (int e = tid; e < C * N * TP; e += NT) {
+      int c, j, p;
+      if (AXIS == 0) { j = e % N; p = (e / N) % TP; c = e / (N * TP); }
+      else { p = e % TP; j = (e / TP) % N; c = e / (TP * N); }
+      cplx v = s[(c * N + j) * TPP + p];
+      if (sc != 1.0) v = sc * v;
+      gout[(long long)c * N3 + tm.off(j, p)] = v;
+    }
+  }
+}

@@ -1,0 +1,71 @@
+// Internal interface between the host driver (pcband.cu) and the kernel translation units.
+#pragma once
+#include <algorithm>
+#include "common.cuh"
+
+#define PC_MAXCOLS 192  // column pointers per launch (Gram T side = [S AS] = 6b, b <= 32)
+
+struct ColPtrs {
+  const cplx* p[PC_MAXCOLS];
+};
+struct MutColPtrs {
+  cplx* p[PC_MAXCOLS];
+};
+
+struct Sym3 {
+  double B[9];  // row-major A^{-1}: B[3*a + i] = b_ai
+  double k[3];
+};
+
+struct EpsCoef {
+  double d[3];  // eps_ii - 1
+  cplx e[3];    // eps_12, eps_13, eps_23
+  int has[3];   // which off-diagonals are non-zero
+};
+
+struct PassArgsH {
+  const cplx* tw;    // tw[j] = exp(-2 pi i j / N)
+  const cplx* ktab;  // symbol pieces, see pointwise.cu
+  double gamma;
+  double scale;
+};
+
+// FFT passes ------------------------------------------------------------------------------
+// kind: 0 plain (C=1), 1 inverse-z with K_A^H prologue (C=3), 2 forward-z with K_A+gamma K_B (C=3)
+// in/out/xh: per-column pointers (xh only for kind 2: the apply's input x_hat), ncols <= PC_MAXCOLS.
+int fft_supported(int n);
+int fft_supported_list(int* sizes, int cap);
+cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
+                            const ColPtrs& xh, int ncols, const PassArgsH& a, cudaStream_t st);
+
+// pointwise ---------------------------------------------------------------------------------
+void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t st);
+void launch_precond(const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const cplx* kt, double gamma,
+                    double thr, cudaStream_t st);
+void launch_eps(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const uint8_t* mask,
+                const EpsCoef& ec, cudaStream_t st);
+int resid_grid(int n);
+void launch_resid(const ColPtrs& X, const ColPtrs& AX, const MutColPtrs& W, const double* lam, int b, int n,
+                  const cplx* kt, double gamma, double thr, int deflate0, double* partial, double* norms,
+                  cudaStream_t st);
+void launch_randn(const MutColPtrs& X, int ncols, long long len, unsigned long long seed, int deflate_stride,
+                  cudaStream_t st);
+
+// dense block algebra ------------------------------------------------------------------------
+// G (p x q, column-major, ld p) = S^H T over rows [0, len): S p columns, T q columns.
+size_t gram_partial_bytes(int p, int q);
+void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
+                 cudaStream_t st);
+// Block update (r <= 32 output columns, C column-major ld = ldc):
+//   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr)
+//   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])
+void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
+                   const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st);
+
+// Rayleigh-Ritz ------------------------------------------------------------------------------
+// G = [G_M | G_A] (p x 2p, column-major ld p).  Outputs C (p x nb, ld p), lambda (nb), info[0] = rank,
+// info[1] = sweeps of the last Jacobi.  Uses scratch (>= 4 p^2 complex).
+void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* lambda, int* info, cplx* scratch,
+               cudaStream_t st);
+// Dense Hermitian eigensolver (one-CTA Jacobi) for tests: A (n x n, ld n) -> w (n, ascending), V (n x n).
+void launch_heevj(const cplx* A, int n, double* w, cplx* V, int* info, cudaStream_t st);

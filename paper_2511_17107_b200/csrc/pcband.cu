@@ -1,0 +1,864 @@
+// libpcband host side: context, C ABI (include/pcband.h) and the LOBPCG driver.
+//
+// Method: Jin & Xie, arXiv 2511.17107.  Per Bloch vector k the driver runs block LOBPCG
+// with soft locking on Op(k) = A_c M A_c^H + gamma B^H B in Fourier coordinates
+// (P:523-529), preconditioned by K_P^{-1}, until Res_j <= tol for the nev smallest pairs
+// (P:1059-1064).  Everything on the data path runs in this library's kernels; the host only decides
+// which columns are still active (one D2H of 2b doubles per iteration) and sequences launches.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/pcband.h"
+#include "kernels.h"
+
+// ------------------------------------------------------------------------------------------
+// errors
+// ------------------------------------------------------------------------------------------
+static thread_local std::string g_err;
+static int set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+#define CU(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      return set_err(e_ == cudaErrorMemoryAllocation ? PC_ENOMEM : PC_ECUDA,          \
+                     std::string(#call) + ": " + cudaGetErrorString(e_));             \
+  } while (0)
+#define CHK(expr)            \
+  do {                       \
+    int rc_ = (expr);        \
+    if (rc_ < 0) return rc_; \
+  } while (0)
+
+extern "C" const char* pc_last_error(void) { return g_err.c_str(); }
+
+// ------------------------------------------------------------------------------------------
+// context
+// ------------------------------------------------------------------------------------------
+struct DevBuf {
+  void* p = nullptr;
+  size_t bytes = 0;
+  int ensure(size_t b) {
+    if (b <= bytes) return PC_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, b);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return set_err(PC_ENOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
+    }
+    bytes = b;
+    return PC_OK;
+  }
+  void release() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+  }
+  template <class T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+struct pc_ctx {
+  int n = 0, device = 0, eps_mode = 1;
+  long long n3 = 0, len = 0;  // N^3, 3 N^3
+  double A[9], B[9];          // row-major; B = A^{-1}
+  double eps[18];
+  double gamma_override = 0.0;
+  int hpd_flags = 0;
+  EpsCoef ec;
+  uint8_t* d_mask = nullptr;
+  cplx* d_tw = nullptr;
+  cplx* d_ktab = nullptr;
+  double cur_k[3] = {NAN, NAN, NAN};
+  double cur_gamma = 0.0, cur_thr = 0.0;
+  DevBuf ws;          // apply workspace
+  int apply_chunk = 0;
+  int guard = 5;
+  double drop_tol = 1e-12;
+  long long kindex_offset = 0;  // global index of kpts[0] (seeds independent of sharding)
+  int verbose = 0;
+  int p_restart = 1;  // drop the P block when the Rayleigh-Ritz basis is rank deficient
+  // LOBPCG storage
+  DevBuf lob, small, gpart;
+  double* h_pinned = nullptr;
+  cudaStream_t stream = nullptr;
+  // profiling
+  int profile = 0;
+  double stat_ms[PC_NSTAT] = {0};
+  double stat_cnt[PC_NSTAT] = {0};
+  std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
+  std::vector<cudaEvent_t> ev_pool;
+};
+
+// ---- profiling helpers (CUDA events on the launching stream) --------------------------------
+static cudaEvent_t ev_get(pc_ctx* c) {
+  if (!c->ev_pool.empty()) {
+    cudaEvent_t e = c->ev_pool.back();
+    c->ev_pool.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  cudaEventCreate(&e);
+  return e;
+}
+struct Prof {
+  pc_ctx* c;
+  int stat;
+  cudaStream_t st;
+  cudaEvent_t e0 = nullptr;
+  Prof(pc_ctx* c_, int s_, cudaStream_t st_) : c(c_), stat(s_), st(st_) {
+    if (c->profile) {
+      e0 = ev_get(c);
+      cudaEventRecord(e0, st);
+    }
+  }
+  ~Prof() {
+    if (c->profile) {
+      cudaEvent_t e1 = ev_get(c);
+      cudaEventRecord(e1, st);
+      c->pending.push_back({stat, {e0, e1}});
+    }
+  }
+};
+static void prof_flush(pc_ctx* c) {
+  for (auto& pe : c->pending) {
+    float ms = 0.f;
+    cudaEventSynchronize(pe.second.second);
+    cudaEventElapsedTime(&ms, pe.second.first, pe.second.second);
+    c->stat_ms[pe.first] += ms;
+    c->stat_cnt[pe.first] += 1;
+    c->ev_pool.push_back(pe.second.first);
+    c->ev_pool.push_back(pe.second.second);
+  }
+  c->pending.clear();
+}
+
+// ---- small host linear algebra -------------------------------------------------------------
+static bool inv3(const double* a, double* b) {
+  double det = a[0] * (a[4] * a[8] - a[5] * a[7]) - a[1] * (a[3] * a[8] - a[5] * a[6]) + a[2] * (a[3] * a[7] - a[4] * a[6]);
+  double sc = 0;
+  for (int i = 0; i < 9; i++) sc = std::fmax(sc, std::fabs(a[i]));
+  if (!(std::fabs(det) > 1e-12 * sc * sc * sc)) return false;
+  b[0] = (a[4] * a[8] - a[5] * a[7]) / det;
+  b[1] = (a[2] * a[7] - a[1] * a[8]) / det;
+  b[2] = (a[1] * a[5] - a[2] * a[4]) / det;
+  b[3] = (a[5] * a[6] - a[3] * a[8]) / det;
+  b[4] = (a[0] * a[8] - a[2] * a[6]) / det;
+  b[5] = (a[2] * a[3] - a[0] * a[5]) / det;
+  b[6] = (a[3] * a[7] - a[4] * a[6]) / det;
+  b[7] = (a[1] * a[6] - a[0] * a[7]) / det;
+  b[8] = (a[0] * a[4] - a[1] * a[3]) / det;
+  return true;
+}
+
+// eigenvalues of a 3x3 Hermitian matrix (complex Jacobi, host)
+static void heev3(const double* e18, double* w) {
+  double ar[3][3], ai[3][3];
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      ar[i][j] = e18[2 * (3 * i + j)];
+      ai[i][j] = e18[2 * (3 * i + j) + 1];
+    }
+  for (int sweep = 0; sweep < 50; sweep++) {
+    double off = 0;
+    for (int p = 0; p < 3; p++)
+      for (int q = p + 1; q < 3; q++) off += ar[p][q] * ar[p][q] + ai[p][q] * ai[p][q];
+    if (off < 1e-34) break;
+    for (int p = 0; p < 3; p++)
+      for (int q = p + 1; q < 3; q++) {
+        double mag = std::hypot(ar[p][q], ai[p][q]);
+        if (mag < 1e-300) continue;
+        double z = (ar[q][q] - ar[p][p]) / (2 * mag);
+        double t = (z >= 0 ? 1.0 : -1.0) / (std::fabs(z) + std::sqrt(1 + z * z));
+        double c = 1 / std::sqrt(1 + t * t), s = t * c;
+        double er = ar[p][q] / mag, ei = ai[p][q] / mag;
+        // A <- U^H A U, U = [[c, s e], [-s conj e, c]] on (p, q)
+        for (int j = 0; j < 3; j++) {  // rows
+          double apr = ar[p][j], api = ai[p][j], aqr = ar[q][j], aqi = ai[q][j];
+          ar[p][j] = c * apr - s * (er * aqr - ei * aqi);
+          ai[p][j] = c * api - s * (er * aqi + ei * aqr);
+          ar[q][j] = s * (er * apr + ei * api) + c * aqr;
+          ai[q][j] = s * (er * api - ei * apr) + c * aqi;
+        }
+        for (int j = 0; j < 3; j++) {  // columns
+          double apr = ar[j][p], api = ai[j][p], aqr = ar[j][q], aqi = ai[j][q];
+          ar[j][p] = c * apr - s * (er * aqr + ei * aqi);
+          ai[j][p] = c * api - s * (er * aqi - ei * aqr);
+          ar[j][q] = s * (er * apr - ei * api) + c * aqr;
+          ai[j][q] = s * (er * api + ei * apr) + c * aqi;
+        }
+      }
+  }
+  for (int i = 0; i < 3; i++) w[i] = ar[i][i];
+}
+
+// ------------------------------------------------------------------------------------------
+// pc_create / destroy / info
+// ------------------------------------------------------------------------------------------
+extern "C" int pc_supported_n(int* sizes, int cap) { return fft_supported_list(sizes, cap); }
+
+extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double eps1[18], const uint8_t* masks,
+                         int eps_mode, double gamma_override, int device) {
+  if (!out || !A || !eps1 || !masks) return set_err(PC_EINVAL, "pc_create: null argument");
+  *out = nullptr;
+  if (!fft_supported(n)) return set_err(PC_EINVAL, "pc_create: unsupported grid size n=" + std::to_string(n));
+  if (eps_mode < 0 || eps_mode > 2) return set_err(PC_EINVAL, "pc_create: bad eps_mode");
+  double B[9];
+  if (!inv3(A, B)) return set_err(PC_EINVAL, "pc_create: lattice matrix A is singular");
+  // Hermitian check
+  double emax = 0;
+  for (int i = 0; i < 18; i++) emax = std::fmax(emax, std::fabs(eps1[i]));
+  for (int i = 0; i < 3; i++)
+    for (int j = 0; j < 3; j++) {
+      double dr = eps1[2 * (3 * i + j)] - eps1[2 * (3 * j + i)];
+      double di = eps1[2 * (3 * i + j) + 1] + eps1[2 * (3 * j + i) + 1];
+      if (std::hypot(dr, di) > 1e-14 * emax) return set_err(PC_EINVAL, "pc_create: eps1 is not Hermitian");
+    }
+  double w[3];
+  heev3(eps1, w);
+  double wmin = std::fmin(w[0], std::fmin(w[1], w[2])), wmax = std::fmax(w[0], std::fmax(w[1], w[2]));
+  if (!(wmin > 0)) return set_err(PC_ENOTPD, "pc_create: eps1 is not positive definite");
+  bool offd = false, zero_off = false;
+  for (int i = 0; i < 3; i++)
+    for (int j = i + 1; j < 3; j++) {
+      bool z = eps1[2 * (3 * i + j)] == 0.0 && eps1[2 * (3 * i + j) + 1] == 0.0;
+      offd |= !z;
+      zero_off |= z;
+    }
+  if (eps_mode == PC_EPS_DIAGONAL && offd)
+    return set_err(PC_EINVAL, "pc_create: PC_EPS_DIAGONAL needs a diagonal eps1");
+  bool sdd = true;
+  for (int i = 0; i < 3; i++) {
+    double s = 0;
+    for (int j = 0; j < 3; j++)
+      if (j != i) s += std::hypot(eps1[2 * (3 * i + j)], eps1[2 * (3 * i + j) + 1]);
+    if (!(eps1[2 * (3 * i + i)] > s)) sdd = false;
+  }
+  bool a1 = wmin > 0 && wmax <= 1.0 + 1e-15;
+
+  cudaError_t e = cudaSetDevice(device);
+  if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("cudaSetDevice: ") + cudaGetErrorString(e));
+  pc_ctx* c = new pc_ctx();
+  c->n = n;
+  c->device = device;
+  c->eps_mode = eps_mode;
+  c->n3 = (long long)n * n * n;
+  c->len = 3 * c->n3;
+  std::memcpy(c->A, A, sizeof(c->A));
+  std::memcpy(c->B, B, sizeof(c->B));
+  std::memcpy(c->eps, eps1, sizeof(c->eps));
+  c->gamma_override = gamma_override;
+  c->hpd_flags = (a1 ? PC_HPD_ASSUMP1 : 0) | (sdd ? PC_HPD_SDD : 0) | (zero_off ? PC_HPD_ZERO_OFFD : 0) |
+                 ((a1 && (sdd || zero_off)) ? PC_HPD_GUARANTEED : 0);
+  for (int i = 0; i < 3; i++) c->ec.d[i] = eps1[2 * (3 * i + i)] - 1.0;
+  const int od[3][2] = {{0, 1}, {0, 2}, {1, 2}};
+  for (int t = 0; t < 3; t++) {
+    int i = od[t][0], j = od[t][1];
+    c->ec.e[t] = mk(eps1[2 * (3 * i + j)], eps1[2 * (3 * i + j) + 1]);
+    c->ec.has[t] = (c->ec.e[t].x != 0.0 || c->ec.e[t].y != 0.0) ? 1 : 0;
+  }
+  auto fail = [&](int code, const std::string& m) {
+    pc_destroy(c);
+    return set_err(code, m);
+  };
+  // masks: pack I1, I2, I3, IV into one byte per point
+  std::vector<uint8_t> packed(c->n3);
+  for (long long i = 0; i < c->n3; i++) {
+    uint8_t b = 0;
+    for (int f = 0; f < 4; f++)
+      if (masks[f * c->n3 + i]) b |= (uint8_t)(1u << f);
+    packed[i] = b;
+  }
+  if (cudaMalloc(&c->d_mask, c->n3) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: mask alloc");
+  if (cudaMemcpy(c->d_mask, packed.data(), c->n3, cudaMemcpyHostToDevice) != cudaSuccess)
+    return fail(PC_ECUDA, "pc_create: mask upload");
+  // twiddles exp(-2 pi i j / N) in long double, rounded once
+  std::vector<cplx> tw(n);
+  const long double PI_L = 3.141592653589793238462643383279502884L;
+  for (int j = 0; j < n; j++) {
+    long double a = -2.0L * PI_L * (long double)j / (long double)n;
+    tw[j] = mk((double)cosl(a), (double)sinl(a));
+    if ((4 * j) % n == 0) {  // exact quarter turns
+      int qd = (4 * j) / n;
+      const double cs[4][2] = {{1, 0}, {0, -1}, {-1, 0}, {0, 1}};
+      tw[j] = mk(cs[qd][0], cs[qd][1]);
+    }
+  }
+  if (cudaMalloc(&c->d_tw, n * sizeof(cplx)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: twiddle alloc");
+  cudaMemcpy(c->d_tw, tw.data(), n * sizeof(cplx), cudaMemcpyHostToDevice);
+  if (cudaMalloc(&c->d_ktab, 9 * n * sizeof(cplx)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: ktab alloc");
+  if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
+    return fail(PC_ECUDA, "pc_create: stream");
+  if (cudaMallocHost(&c->h_pinned, 4096 * sizeof(double)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: pinned");
+  *out = c;
+  return PC_OK;
+}
+
+extern "C" void pc_destroy(pc_ctx* c) {
+  if (!c) return;
+  cudaSetDevice(c->device);
+  if (c->stream) cudaStreamSynchronize(c->stream);
+  prof_flush(c);
+  for (auto e : c->ev_pool) cudaEventDestroy(e);
+  if (c->d_mask) cudaFree(c->d_mask);
+  if (c->d_tw) cudaFree(c->d_tw);
+  if (c->d_ktab) cudaFree(c->d_ktab);
+  c->ws.release();
+  c->lob.release();
+  c->small.release();
+  c->gpart.release();
+  if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->stream) cudaStreamDestroy(c->stream);
+  delete c;
+}
+
+static double gamma_rule(const pc_ctx* c, const double k[3]) {
+  if (c->gamma_override > 0) return c->gamma_override;
+  // practical penalty
+  const double fourpi2 = 4.0 * M_PI * M_PI;
+  double nk = std::sqrt(k[0] * k[0] + k[1] * k[1] + k[2] * k[2]);
+  if (nk == 0.0 || nk >= 1.0) return fourpi2;
+  return fourpi2 / (nk * nk);
+}
+
+extern "C" double pc_gamma(const pc_ctx* c, const double k[3]) { return (c && k) ? gamma_rule(c, k) : NAN; }
+
+extern "C" int pc_info(const pc_ctx* c, int* hpd_flags, size_t* ws_bytes_per_col) {
+  if (!c) return set_err(PC_EINVAL, "pc_info: null ctx");
+  if (hpd_flags) *hpd_flags = c->hpd_flags;
+  if (ws_bytes_per_col) *ws_bytes_per_col = (size_t)c->len * sizeof(cplx);
+  return PC_OK;
+}
+
+extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
+  if (!c || !key) return set_err(PC_EINVAL, "pc_set_option: null");
+  std::string k(key);
+  if (k == "guard") { if (v < 0 || v > 32) return set_err(PC_EINVAL, "guard out of range"); c->guard = (int)v; }
+  else if (k == "apply_chunk") c->apply_chunk = (int)v;
+  else if (k == "profile") c->profile = v != 0.0;
+  else if (k == "drop_tol") c->drop_tol = v;
+  else if (k == "kindex_offset") c->kindex_offset = (long long)v;
+  else if (k == "verbose") c->verbose = (int)v;
+  else if (k == "p_restart") c->p_restart = (int)v;
+  else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
+  return PC_OK;
+}
+
+extern "C" int pc_stats(pc_ctx* c, double* out, int reset) {
+  if (!c) return set_err(PC_EINVAL, "pc_stats: null ctx");
+  cudaSetDevice(c->device);
+  prof_flush(c);
+  if (out)
+    for (int i = 0; i < PC_NSTAT; i++) {
+      out[2 * i] = c->stat_cnt[i];
+      out[2 * i + 1] = c->stat_ms[i];
+    }
+  if (reset)
+    for (int i = 0; i < PC_NSTAT; i++) c->stat_cnt[i] = c->stat_ms[i] = 0;
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// symbols for k (stream-ordered; cached while k is unchanged)
+// ------------------------------------------------------------------------------------------
+static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
+  c->cur_gamma = gamma_rule(c, k);
+  if (k[0] == c->cur_k[0] && k[1] == c->cur_k[1] && k[2] == c->cur_k[2]) return;
+  Sym3 s;
+  std::memcpy(s.B, c->B, sizeof(s.B));
+  for (int i = 0; i < 3; i++) s.k[i] = k[i];
+  launch_ktab(c->d_ktab, c->d_tw, c->n, s, st);
+  // |kappa|^2 <= 1e-28 max|kappa|^2 -> pass-through (reading R7); max bounded via the 1-D pieces
+  double bound = 0;
+  const double n = c->n;
+  for (int i = 0; i < 3; i++) {
+    double m = 0;
+    for (int a = 0; a < 3; a++) m += std::fabs(c->B[3 * a + i]) * 2.0 * n;
+    m += std::fabs(k[i]);
+    bound += m * m;
+  }
+  c->cur_thr = 1e-28 * bound;
+  for (int i = 0; i < 3; i++) c->cur_k[i] = k[i];
+}
+
+// ------------------------------------------------------------------------------------------
+// apply
+// ------------------------------------------------------------------------------------------
+static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
+                    const ColPtrs& xh, int nc, double scale, cudaStream_t st) {
+  PassArgsH a;
+  a.tw = c->d_tw;
+  a.ktab = c->d_ktab;
+  a.gamma = c->cur_gamma;
+  a.scale = scale;
+  cudaError_t e = launch_fft_pass(c->n, axis, dir, kind, in, out, xh, nc, a, st);
+  if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("fft pass: ") + cudaGetErrorString(e));
+  return PC_OK;
+}
+
+static ColPtrs to_const(const MutColPtrs& m, int nc) {
+  ColPtrs r;
+  for (int i = 0; i < nc; i++) r.p[i] = m.p[i];
+  return r;
+}
+
+// Fourier-space apply of nc <= PC_MAXCOLS columns: Y = Op X, ws = nc workspace columns.
+static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const MutColPtrs& WS, int nc,
+                         cudaStream_t st) {
+  const int n = c->n;
+  const double inv_n3 = 1.0 / ((double)n * n * n);
+  ColPtrs Yc = to_const(Y, nc), Wc = to_const(WS, nc), none{};
+  {
+    Prof p(c, PC_STAT_FFT_Z_KAH, st);
+    CHK(fft_pass(c, 2, +1, 1, X, Y, none, nc, inv_n3, st));
+  }
+  {
+    Prof p(c, PC_STAT_FFT_MID, st);
+    CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
+    CHK(fft_pass(c, 0, +1, 0, Yc, Y, none, nc, 1.0, st));
+  }
+  {
+    Prof p(c, PC_STAT_EPS, st);
+    launch_eps(c->eps_mode, Yc, WS, nc, n, c->d_mask, c->ec, st);
+  }
+  {
+    Prof p(c, PC_STAT_FFT_MID, st);
+    CHK(fft_pass(c, 0, -1, 0, Wc, WS, none, nc, 1.0, st));
+    CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
+  }
+  {
+    Prof p(c, PC_STAT_FFT_Z_KA, st);
+    CHK(fft_pass(c, 2, -1, 2, Wc, Y, X, nc, 1.0, st));
+  }
+  return PC_OK;
+}
+
+// unitary 3-D DFT per component; dir = -1: F3^H (to Fourier), +1: F3 (to real).  Y may equal X.
+static int fft3(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, int nc, int dir, cudaStream_t st) {
+  const double s = 1.0 / std::sqrt((double)c->n);
+  ColPtrs Yc = to_const(Y, nc), none{};
+  Prof p(c, PC_STAT_FFT_MID, st);
+  CHK(fft_pass(c, 0, dir, 0, X, Y, none, nc, s, st));
+  CHK(fft_pass(c, 1, dir, 0, Yc, Y, none, nc, s, st));
+  CHK(fft_pass(c, 2, dir, 0, Yc, Y, none, nc, s, st));
+  return PC_OK;
+}
+
+static int ensure_ws(pc_ctx* c, int cols) {
+  size_t need = (size_t)cols * c->len * sizeof(cplx);
+  if (need <= c->ws.bytes) return PC_OK;
+  cudaDeviceSynchronize();
+  return c->ws.ensure(need);
+}
+
+static int chunk_cols(pc_ctx* c, int ncols, int per_call_max) {
+  int ch = std::min(ncols, per_call_max);
+  if (c->apply_chunk > 0) ch = std::min(ch, c->apply_chunk);
+  return std::max(ch, 1);
+}
+
+static int apply_cols(pc_ctx* c, const double k[3], const ColPtrs& X, const MutColPtrs& Y, int ncols, int space,
+                      cudaStream_t st) {
+  set_k(c, k, st);
+  const int ch = chunk_cols(c, ncols, 64);
+  const int nws = (space == PC_SPACE_REAL) ? 2 * ch : ch;
+  CHK(ensure_ws(c, nws));
+  cplx* ws = c->ws.as<cplx>();
+  for (int j0 = 0; j0 < ncols; j0 += ch) {
+    int nc = std::min(ch, ncols - j0);
+    ColPtrs x;
+    MutColPtrs y, w, w2;
+    for (int j = 0; j < nc; j++) {
+      x.p[j] = X.p[j0 + j];
+      y.p[j] = Y.p[j0 + j];
+      w.p[j] = ws + (size_t)j * c->len;
+      w2.p[j] = ws + (size_t)(ch + j) * c->len;
+    }
+    if (space == PC_SPACE_FOURIER) {
+      CHK(apply_fourier(c, x, y, w, nc, st));
+    } else {
+      CHK(fft3(c, x, w2, nc, -1, st));                 // xhat = F3^H H
+      CHK(apply_fourier(c, to_const(w2, nc), y, w, nc, st));
+      CHK(fft3(c, to_const(y, nc), y, nc, +1, st));    // back to real space
+    }
+  }
+  return PC_OK;
+}
+
+static void block_ptrs(const void* base, long long ld, int j0, int nc, ColPtrs& out) {
+  const cplx* b = reinterpret_cast<const cplx*>(base);
+  for (int j = 0; j < nc; j++) out.p[j] = b + (size_t)(j0 + j) * ld;
+}
+static void block_ptrs(void* base, long long ld, int j0, int nc, MutColPtrs& out) {
+  cplx* b = reinterpret_cast<cplx*>(base);
+  for (int j = 0; j < nc; j++) out.p[j] = b + (size_t)(j0 + j) * ld;
+}
+
+static int check_block(pc_ctx* c, const void* X, const void* Y, int ncols, long long ld, const char* who) {
+  if (!c) return set_err(PC_EINVAL, std::string(who) + ": null ctx");
+  if (ncols < 0) return set_err(PC_EINVAL, std::string(who) + ": ncols < 0");
+  if (ncols > 0 && (!X || !Y)) return set_err(PC_EINVAL, std::string(who) + ": null data pointer");
+  if (ld < c->len) return set_err(PC_EINVAL, std::string(who) + ": ld < 3 N^3");
+  return PC_OK;
+}
+
+extern "C" int pc_apply(pc_ctx* c, const double k[3], const void* X, void* Y, int ncols, long long ld, int space,
+                        void* stream) {
+  CHK(check_block(c, X, Y, ncols, ld, "pc_apply"));
+  if (!k) return set_err(PC_EINVAL, "pc_apply: null k");
+  if (space != PC_SPACE_FOURIER && space != PC_SPACE_REAL) return set_err(PC_EINVAL, "pc_apply: bad space");
+  if (X == Y && ncols > 0) return set_err(PC_EINVAL, "pc_apply: X and Y alias");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int j0 = 0; j0 < ncols; j0 += PC_MAXCOLS) {
+    int nc = std::min(PC_MAXCOLS, ncols - j0);
+    ColPtrs x;
+    MutColPtrs y;
+    block_ptrs(X, ld, j0, nc, x);
+    block_ptrs(Y, ld, j0, nc, y);
+    CHK(apply_cols(c, k, x, y, nc, space, st));
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+extern "C" int pc_precond(pc_ctx* c, const double k[3], const void* R, void* P, int ncols, long long ld,
+                          void* stream) {
+  CHK(check_block(c, R, P, ncols, ld, "pc_precond"));
+  if (!k) return set_err(PC_EINVAL, "pc_precond: null k");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  set_k(c, k, st);
+  for (int j0 = 0; j0 < ncols; j0 += PC_MAXCOLS) {
+    int nc = std::min(PC_MAXCOLS, ncols - j0);
+    ColPtrs r;
+    MutColPtrs p;
+    block_ptrs(R, ld, j0, nc, r);
+    block_ptrs(P, ld, j0, nc, p);
+    Prof pf(c, PC_STAT_RESID, st);
+    launch_precond(r, p, nc, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, st);
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+extern "C" int pc_apply_eps(pc_ctx* c, const void* E, void* Y, int ncols, long long ld, void* stream) {
+  CHK(check_block(c, E, Y, ncols, ld, "pc_apply_eps"));
+  if (E == Y && ncols > 0) return set_err(PC_EINVAL, "pc_apply_eps: E and Y alias");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int j0 = 0; j0 < ncols; j0 += PC_MAXCOLS) {
+    int nc = std::min(PC_MAXCOLS, ncols - j0);
+    ColPtrs e;
+    MutColPtrs y;
+    block_ptrs(E, ld, j0, nc, e);
+    block_ptrs(Y, ld, j0, nc, y);
+    Prof pf(c, PC_STAT_EPS, st);
+    launch_eps(c->eps_mode, e, y, nc, c->n, c->d_mask, c->ec, st);
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+extern "C" int pc_fft3(pc_ctx* c, const void* X, void* Y, int ncols, long long ld, int direction, void* stream) {
+  CHK(check_block(c, X, Y, ncols, ld, "pc_fft3"));
+  if (direction != PC_FFT_TO_FOURIER && direction != PC_FFT_TO_REAL) return set_err(PC_EINVAL, "pc_fft3: direction");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int j0 = 0; j0 < ncols; j0 += PC_MAXCOLS) {
+    int nc = std::min(PC_MAXCOLS, ncols - j0);
+    ColPtrs x;
+    MutColPtrs y;
+    block_ptrs(X, ld, j0, nc, x);
+    block_ptrs(Y, ld, j0, nc, y);
+    CHK(fft3(c, x, y, nc, direction == PC_FFT_TO_FOURIER ? -1 : +1, st));
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+// debug entry: one FFT pass (kind 0 plain / 1 K_A^H-fused inverse z / 2 K_A+gamma K_B forward z)
+extern "C" int pc_debug_pass(pc_ctx* c, const double k[3], int kind, int axis, int dir, const void* X, void* Y,
+                             const void* XH, int ncols, long long ld, double scale) {
+  CHK(check_block(c, X, Y, ncols, ld, "pc_debug_pass"));
+  CU(cudaSetDevice(c->device));
+  set_k(c, k, 0);
+  ColPtrs x, xh;
+  MutColPtrs y;
+  block_ptrs(X, ld, 0, ncols, x);
+  block_ptrs(Y, ld, 0, ncols, y);
+  if (XH) block_ptrs(XH, ld, 0, ncols, xh);
+  CHK(fft_pass(c, axis, dir, kind, x, y, xh, ncols, scale, 0));
+  CU(cudaDeviceSynchronize());
+  return PC_OK;
+}
+
+// debug entry used by the tests: dense Hermitian eigensolver on device (host in/out)
+extern "C" int pc_debug_heevj(const double* A_host, int n, double* w_host, double* V_host, int* sweeps) {
+  if (n < 1 || n > 80) return set_err(PC_EINVAL, "pc_debug_heevj: 1 <= n <= 80");
+  cplx *dA, *dV;
+  double* dw;
+  int* di;
+  CU(cudaMalloc(&dA, n * n * sizeof(cplx)));
+  CU(cudaMalloc(&dV, n * n * sizeof(cplx)));
+  CU(cudaMalloc(&dw, n * sizeof(double)));
+  CU(cudaMalloc(&di, sizeof(int)));
+  CU(cudaMemcpy(dA, A_host, n * n * sizeof(cplx), cudaMemcpyHostToDevice));
+  launch_heevj(dA, n, dw, dV, di, 0);
+  CU(cudaDeviceSynchronize());
+  CU(cudaMemcpy(w_host, dw, n * sizeof(double), cudaMemcpyDeviceToHost));
+  if (V_host) CU(cudaMemcpy(V_host, dV, n * n * sizeof(cplx), cudaMemcpyDeviceToHost));
+  if (sweeps) CU(cudaMemcpy(sweeps, di, sizeof(int), cudaMemcpyDeviceToHost));
+  cudaFree(dA);
+  cudaFree(dV);
+  cudaFree(dw);
+  cudaFree(di);
+  return PC_OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// LOBPCG (pc_bands)
+// ------------------------------------------------------------------------------------------
+__global__ void normalize_copy_kernel(ColPtrs X, const double* norms, MutColPtrs Y, long long len) {
+  const int j = blockIdx.y;
+  const double s = 1.0 / sqrt(norms[2 * j + 1]);
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x)
+    Y.p[j][i] = s * X.p[j][i];
+}
+
+static unsigned long long mix64(unsigned long long x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, int maxit, unsigned long long seed,
+                   double* omega2, double* resid, int* iters, int* status, cplx* evec_out) {
+  cudaStream_t st = c->stream;
+  const int b = nev + c->guard;
+  const long long len = c->len;
+  const int maxp = 3 * b;
+  set_k(c, k, st);
+  const bool deflate = (k[0] == 0.0 && k[1] == 0.0 && k[2] == 0.0);
+
+  // ---- storage: 10 b columns + apply workspace b columns
+  const size_t colb = (size_t)len * sizeof(cplx);
+  CHK(c->lob.ensure(10 * (size_t)b * colb));
+  CHK(ensure_ws(c, b));
+  cplx* base = c->lob.as<cplx>();
+  auto col = [&](int slot, int j) { return base + ((size_t)slot * b + j) * len; };
+  enum { XA = 0, AXA, XB, AXB, PA, APA, PB, APB, WW, AWW };
+  int sX = XA, sAX = AXA, sXn = XB, sAXn = AXB, sP = PA, sAP = APA, sPn = PB, sAPn = APB;
+  // small device buffers: G (maxp x 2maxp), C (maxp x b), lam, info, rr scratch, resid partials, norms
+  const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)2 * maxp * 80;
+  const int rg = resid_grid(c->n);
+  size_t small_bytes = (nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) + 64;
+  CHK(c->small.ensure(small_bytes));
+  CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
+  cplx* dG = c->small.as<cplx>();
+  cplx* dC = dG + nG;
+  cplx* dScr = dC + nC;
+  double* dLam = reinterpret_cast<double*>(dScr + nScr);
+  double* dNorm = dLam + b;
+  double* dPart = dNorm + 2 * b;
+  int* dInfo = reinterpret_cast<int*>(dPart + (size_t)rg * b * 2);
+  double* hN = c->h_pinned;                 // 2b norms
+  int* hInfo = reinterpret_cast<int*>(c->h_pinned + 2048);
+  MutColPtrs wsp;
+  for (int j = 0; j < b; j++) wsp.p[j] = c->ws.as<cplx>() + (size_t)j * len;
+
+  auto mcols = [&](int slot, const std::vector<int>& js, MutColPtrs& m, int off) {
+    for (size_t t = 0; t < js.size(); t++) m.p[off + t] = col(slot, js[t]);
+  };
+  auto ccols = [&](int slot, const std::vector<int>& js, ColPtrs& m, int off) {
+    for (size_t t = 0; t < js.size(); t++) m.p[off + t] = col(slot, js[t]);
+  };
+  std::vector<int> all(b);
+  for (int j = 0; j < b; j++) all[j] = j;
+
+  auto apply_list = [&](int src, int dst, const std::vector<int>& js) -> int {
+    ColPtrs x;
+    MutColPtrs y;
+    ccols(src, js, x, 0);
+    mcols(dst, js, y, 0);
+    MutColPtrs w;
+    for (size_t t = 0; t < js.size(); t++) w.p[t] = wsp.p[t];
+    return apply_fourier(c, x, y, w, (int)js.size(), st);
+  };
+  auto rr = [&](int p) -> int {
+    {
+      Prof pf(c, PC_STAT_RR, st);
+      launch_rr(dG, p, b, c->drop_tol, dC, dLam, dInfo, dScr, st);
+    }
+    cudaMemcpyAsync(hInfo, dInfo, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("rayleigh-ritz: ") + cudaGetErrorString(e));
+    return hInfo[0];  // rank
+  };
+
+  // ---- start block X0 (counter-based Gaussian), AX0, Rayleigh-Ritz on span(X0)
+  {
+    Prof pf(c, PC_STAT_OTHER, st);
+    MutColPtrs x0;
+    mcols(sX, all, x0, 0);
+    launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)kidx), deflate ? (int)c->n3 : 0, st);
+  }
+  CHK(apply_list(sX, sAX, all));
+  {
+    ColPtrs S, T;
+    ccols(sX, all, S, 0);
+    ccols(sX, all, T, 0);
+    ccols(sAX, all, T, b);
+    Prof pf(c, PC_STAT_GRAM, st);
+    launch_gram(S, b, T, 2 * b, len, dG, c->gpart.as<cplx>(), st);
+  }
+  int rank = rr(b);
+  if (rank < b) return set_err(PC_ENUMERIC, "pc_bands: start block is rank deficient");
+  {
+    Prof pf(c, PC_STAT_UPDATE, st);
+    ColPtrs S;
+    MutColPtrs Y;
+    ccols(sX, all, S, 0);
+    mcols(sXn, all, Y, 0);
+    launch_update(S, b, dC, b, b, b, nullptr, Y, nullptr, len, st);
+    ccols(sAX, all, S, 0);
+    mcols(sAXn, all, Y, 0);
+    launch_update(S, b, dC, b, b, b, nullptr, Y, nullptr, len, st);
+  }
+  std::swap(sX, sXn);
+  std::swap(sAX, sAXn);
+
+  std::vector<char> active(b, 1);
+  std::vector<double> res(b, 0.0);
+  bool haveP = false;
+  int it = 0, conv = 0;
+  for (;; it++) {
+    // residuals, K_P^{-1} R for every column
+    {
+      Prof pf(c, PC_STAT_RESID, st);
+      ColPtrs X, AX;
+      MutColPtrs W;
+      ccols(sX, all, X, 0);
+      ccols(sAX, all, AX, 0);
+      mcols(WW, all, W, 0);
+      launch_resid(X, AX, W, dLam, b, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dNorm, st);
+    }
+    cudaMemcpyAsync(hN, dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
+    {
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("lobpcg: ") + cudaGetErrorString(e));
+    }
+    if (c->profile) prof_flush(c);
+    conv = 1;
+    for (int j = 0; j < b; j++) {
+      res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
+      if (!(res[j] > tol)) active[j] = 0;  // soft locking: once converged, stays locked
+      if (j < nev && res[j] > tol) conv = 0;
+    }
+    if (c->verbose) {
+      fprintf(stderr, "[pcband] k%d it %d rank %d res:", kidx, it, rank);
+      for (int j = 0; j < b; j++) fprintf(stderr, " %.2e%s", res[j], active[j] ? "" : "*");
+      fprintf(stderr, "\n");
+    }
+    if (conv || it >= maxit) break;
+    std::vector<int> act;
+    for (int j = 0; j < b; j++)
+      if (active[j]) act.push_back(j);
+    const int na = (int)act.size();
+    if (na == 0) break;
+    CHK(apply_list(WW, AWW, act));
+    int p = 0;
+    for (int attempt = 0; attempt < 2; attempt++) {
+      p = b + na + (haveP ? na : 0);
+      ColPtrs S, T;
+      ccols(sX, all, S, 0);
+      ccols(WW, act, S, b);
+      if (haveP) ccols(sP, act, S, b + na);
+      for (int t = 0; t < p; t++) T.p[t] = S.p[t];
+      ccols(sAX, all, T, p);
+      ccols(AWW, act, T, p + b);
+      if (haveP) ccols(sAP, act, T, p + b + na);
+      {
+        Prof pf(c, PC_STAT_GRAM, st);
+        launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
+      }
+      rank = rr(p);
+      if (rank >= p || (rank >= b && !c->p_restart)) break;
+      if (rank >= b && !haveP) break;
+      if (!haveP) return set_err(PC_ENUMERIC, "pc_bands: Rayleigh-Ritz basis collapsed (rank " +
+                                                  std::to_string(rank) + " < " + std::to_string(b) + ")");
+      haveP = false;  // restart without the P block
+    }
+    // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images
+    {
+      Prof pf(c, PC_STAT_UPDATE, st);
+      ColPtrs S;
+      MutColPtrs Y1, Y2;
+      ccols(sX, all, S, 0);
+      ccols(WW, act, S, b);
+      if (haveP) ccols(sP, act, S, b + na);
+      mcols(sPn, all, Y1, 0);
+      mcols(sXn, all, Y2, 0);
+      launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
+      ccols(sAX, all, S, 0);
+      ccols(AWW, act, S, b);
+      if (haveP) ccols(sAP, act, S, b + na);
+      mcols(sAPn, all, Y1, 0);
+      mcols(sAXn, all, Y2, 0);
+      launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
+    }
+    std::swap(sX, sXn);
+    std::swap(sAX, sAXn);
+    std::swap(sP, sPn);
+    std::swap(sAP, sAPn);
+    haveP = true;
+  }
+  // outputs
+  cudaMemcpyAsync(hN + 2 * b, dLam, b * sizeof(double), cudaMemcpyDeviceToHost, st);
+  if (evec_out) {
+    ColPtrs X;
+    MutColPtrs Y;
+    for (int j = 0; j < nev; j++) {
+      X.p[j] = col(sX, j);
+      Y.p[j] = evec_out + (size_t)j * len;
+    }
+    normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, st>>>(X, dNorm, Y, len);
+  }
+  CU(cudaStreamSynchronize(st));
+  if (c->profile) prof_flush(c);
+  for (int j = 0; j < nev; j++) {
+    omega2[j] = hN[2 * b + j];
+    if (resid) resid[j] = res[j];
+  }
+  if (iters) *iters = it;
+  if (status) *status = conv ? 0 : 1;
+  return conv ? PC_OK : PC_ENOTCONV;
+}
+
+extern "C" int pc_bands(pc_ctx* c, const double* kpts, int nk, int nev, double tol, int maxit,
+                        unsigned long long seed, double* omega2, double* resid, int* iters, int* status, void* evecs) {
+  if (!c || (!kpts && nk > 0) || (!omega2 && nk > 0)) return set_err(PC_EINVAL, "pc_bands: null argument");
+  if (nk < 0 || nev < 1 || !(tol > 0) || maxit < 0) return set_err(PC_EINVAL, "pc_bands: bad sizes/tol");
+  const int b = nev + c->guard;
+  if (3 * b > 80) return set_err(PC_EINVAL, "pc_bands: nev + guard must be <= 26");
+  CU(cudaSetDevice(c->device));
+  int rc_all = PC_OK;
+  for (int i = 0; i < nk; i++) {
+    cplx* ev = evecs ? reinterpret_cast<cplx*>(evecs) + (size_t)i * nev * c->len : nullptr;
+    int st_i = 0, it_i = 0;
+    int rc = solve_k(c, kpts + 3 * i, (int)(c->kindex_offset + i), nev, tol, maxit, seed, omega2 + (size_t)i * nev,
+                     resid ? resid + (size_t)i * nev : nullptr, &it_i, &st_i, ev);
+    if (rc < 0) return rc;
+    if (iters) iters[i] = it_i;
+    if (status) status[i] = st_i;
+    if (rc == PC_ENOTCONV) rc_all = PC_ENOTCONV;
+  }
+  return rc_all;
+}

@@ -1,0 +1,269 @@
+// On-device Rayleigh-Ritz for LOBPCG: one CTA solves the small projected
+// generalized Hermitian eigenproblem  G_A c = theta G_M c  (p <= RR_MAXN) by
+//   1. symmetric scaling D = diag(G_M)^{-1/2};
+//   2. Jacobi eigendecomposition D G_M D = V Sigma V^H, dropping directions with
+//      sigma < drop_tol * sigma_max (rank-revealing, SVQB-style);
+//   3. T = D V_r Sigma_r^{-1/2}, H = T^H G_A T;
+//   4. Jacobi eigendecomposition H = Q Theta Q^H, ascending;
+//   5. C = T Q[:, :nb], lambda = Theta[:nb].
+// Cyclic parallel Jacobi with a round-robin (tournament) pairing: per round np/2 disjoint complex
+// rotations U = [[c, s e], [-s conj(e), c]] (e = a_pq/|a_pq|) are applied as 2x2 blocks
+// U_i^H A_{ii'} U_{i'} (one barrier per round) and accumulated into V.
+#include "kernels.h"
+
+constexpr int RR_MAXN = 80;
+constexpr int RR_THREADS = 512;
+
+struct JacSm {
+  int P[RR_MAXN / 2], Q[RR_MAXN / 2];
+  double c[RR_MAXN / 2], s[RR_MAXN / 2];
+  cplx e[RR_MAXN / 2];
+  int nrot;
+};
+
+DEV void tpair(int r, int i, int m, int& P, int& Q) {
+  int a, b;
+  if (i == 0) { a = 0; b = 1 + r % (m - 1); }
+  else { a = 1 + (r + i) % (m - 1); b = 1 + (r - i + m - 1) % (m - 1); }
+  P = min(a, b);
+  Q = max(a, b);
+}
+
+// A, V column-major with leading dimension ld (= np).  A Hermitian n x n zero-padded to np (even).
+DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps) {
+  const int tid = threadIdx.x;
+  const int h = np / 2;
+  int sweep = 0;
+  for (; sweep < max_sweeps; sweep++) {
+    if (tid == 0) js.nrot = 0;
+    __syncthreads();
+    for (int r = 0; r < np - 1; r++) {
+      for (int i = tid; i < h; i += blockDim.x) {
+        int P, Q;
+        tpair(r, i, np, P, Q);
+        double c = 1.0, s = 0.0;
+        cplx e = mk(1.0, 0.0);
+        if (Q < n) {
+          cplx apq = A[P + Q * ld];
+          double mag = hypot(apq.x, apq.y);
+          double app = A[P + P * ld].x, aqq = A[Q + Q * ld].x;
+          if (mag > 1e-300 && mag > 1e-16 * sqrt(fabs(app * aqq))) {
+            double z = (aqq - app) / (2.0 * mag);
+            double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
+            c = 1.0 / sqrt(1.0 + t * t);
+            s = t * c;
+            e = mk(apq.x / mag, apq.y / mag);
+            atomicAdd(&js.nrot, 1);
+          }
+        }
+        js.P[i] = P; js.Q[i] = Q; js.c[i] = c; js.s[i] = s; js.e[i] = e;
+      }
+      __syncthreads();
+      for (int it = tid; it < h * h; it += blockDim.x) {
+        const int i = it % h, i2 = it / h;
+        const double c = js.c[i], s = js.s[i], c2 = js.c[i2], s2 = js.s[i2];
+        if (s == 0.0 && s2 == 0.0) continue;
+        const int P = js.P[i], Q = js.Q[i], P2 = js.P[i2], Q2 = js.Q[i2];
+        const cplx e = js.e[i], e2 = js.e[i2];
+        cplx m00 = A[P + P2 * ld], m01 = A[P + Q2 * ld], m10 = A[Q + P2 * ld], m11 = A[Q + Q2 * ld];
+        // L = U_i^H M
+        cplx se = s * e, sec = s * conjg(e);
+        cplx l00 = c * m00 - cmul(se, m10), l01 = c * m01 - cmul(se, m11);
+        cplx l10 = cmul(sec, m00) + c * m10, l11 = cmul(sec, m01) + c * m11;
+        // R = L U_i2
+        cplx se2 = s2 * e2, sec2 = s2 * conjg(e2);
+        A[P + P2 * ld] = c2 * l00 - cmul(sec2, l01);
+        A[P + Q2 * ld] = cmul(se2, l00) + c2 * l01;
+        A[Q + P2 * ld] = c2 * l10 - cmul(sec2, l11);
+        A[Q + Q2 * ld] = cmul(se2, l10) + c2 * l11;
+      }
+      for (int it = tid; it < np * h; it += blockDim.x) {
+        const int j = it % np, i = it / np;
+        const double s = js.s[i];
+        if (s == 0.0) continue;
+        const double c = js.c[i];
+        const int P = js.P[i], Q = js.Q[i];
+        const cplx e = js.e[i];
+        cplx a = V[j + P * ld], b = V[j + Q * ld];
+        V[j + P * ld] = c * a - cmul(s * conjg(e), b);
+        V[j + Q * ld] = cmul(s * e, a) + c * b;
+      }
+      __syncthreads();
+    }
+    const int nr = js.nrot;
+    __syncthreads();
+    if (nr == 0) break;
+  }
+  return sweep;
+}
+
+// rank[i] = position of w[i] in ascending order (ties by index); valid for i < n
+DEV void rank_sort(const double* w, int n, int* order) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    int r = 0;
+    double wi = w[i];
+    for (int j = 0; j < n; j++) r += (w[j] < wi) || (w[j] == wi && j < i);
+    order[r] = i;
+  }
+}
+
+__global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__ G, int p, int nb, double drop_tol,
+                                                        cplx* Cout, double* lam, int* info, cplx* scratch) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const int np = (p + 1) & ~1, ld = np;
+  cplx* A = reinterpret_cast<cplx*>(rsm);
+  cplx* V = A + np * np;
+  __shared__ JacSm js;
+  __shared__ double dsc[RR_MAXN], sig[RR_MAXN];
+  __shared__ int keep[RR_MAXN], order[RR_MAXN];
+  __shared__ int rank_sh;
+  const int tid = threadIdx.x;
+  const cplx* GM = G;
+  const cplx* GA = G + (size_t)p * p;
+
+  // 1. scaling
+  for (int i = tid; i < p; i += blockDim.x) {
+    double d = GM[i + (size_t)i * p].x;
+    dsc[i] = d > 0.0 ? 1.0 / sqrt(d) : 0.0;
+  }
+  __syncthreads();
+  for (int e = tid; e < np * np; e += blockDim.x) {
+    int i = e % np, j = e / np;
+    cplx v = mk(0, 0);
+    if (i < p && j < p) v = (dsc[i] * dsc[j]) * GM[i + (size_t)j * p];
+    if (i == j && i < p) v.y = 0.0;
+    A[e] = v;
+    V[e] = mk(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  // 2. eig of scaled G_M
+  jacobi_smem(A, V, p, np, ld, js, 40);
+  for (int i = tid; i < p; i += blockDim.x) sig[i] = A[i + i * ld].x;
+  __syncthreads();
+  if (tid == 0) {
+    double smax = 0.0;
+    for (int i = 0; i < p; i++) smax = fmax(smax, sig[i]);
+    int r = 0;
+    for (int i = 0; i < p; i++)
+      if (sig[i] > drop_tol * smax) keep[r++] = i;
+    rank_sh = r;
+  }
+  __syncthreads();
+  const int r = rank_sh;
+  // 3. T = D V_r Sigma_r^{-1/2}  -> scratch T (p x r, ld p)
+  cplx* T = scratch;
+  cplx* U = scratch + (size_t)p * RR_MAXN;
+  for (int e = tid; e < p * r; e += blockDim.x) {
+    int i = e % p, t = e / p;
+    int kk = keep[t];
+    T[i + (size_t)t * p] = (dsc[i] / sqrt(sig[kk])) * V[i + kk * ld];
+  }
+  __syncthreads();
+  // U = G_A T (p x r)
+  for (int e = tid; e < p * r; e += blockDim.x) {
+    int i = e % p, t = e / p;
+    cplx acc = mk(0, 0);
+    for (int j = 0; j < p; j++) acc = cfma(GA[i + (size_t)j * p], T[j + (size_t)t * p], acc);
+    U[i + (size_t)t * p] = acc;
+  }
+  __syncthreads();
+  // H = T^H U (r x r) -> A (padded to rp), V = I
+  const int rp = (r + 1) & ~1;
+  for (int e = tid; e < rp * rp; e += blockDim.x) {
+    int i = e % rp, j = e / rp;
+    cplx v = mk(0, 0);
+    if (i < r && j < r) {
+      for (int k = 0; k < p; k++) v = v + cmulc(T[k + (size_t)i * p], U[k + (size_t)j * p]);
+    }
+    A[i + j * rp] = v;
+    V[i + j * rp] = mk(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  // Hermitian symmetrisation (rounding): A <- (A + A^H)/2
+  for (int e = tid; e < r * r; e += blockDim.x) {
+    int i = e % r, j = e / r;
+    if (i < j) {
+      cplx a = A[i + j * rp], b = A[j + i * rp];
+      cplx m = mk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      A[i + j * rp] = m;
+      A[j + i * rp] = conjg(m);
+    } else if (i == j) {
+      A[i + i * rp].y = 0.0;
+    }
+  }
+  __syncthreads();
+  // 4. eig of H
+  int sw = jacobi_smem(A, V, r, rp, rp, js, 40);
+  for (int i = tid; i < r; i += blockDim.x) sig[i] = A[i + i * rp].x;
+  __syncthreads();
+  rank_sort(sig, r, order);
+  __syncthreads();
+  // 5. C = T Q[:, order[:nb]]
+  const int nout = min(nb, r);
+  for (int e = tid; e < p * nout; e += blockDim.x) {
+    int i = e % p, t = e / p;
+    int kk = order[t];
+    cplx acc = mk(0, 0);
+    for (int j = 0; j < r; j++) acc = cfma(T[i + (size_t)j * p], V[j + kk * rp], acc);
+    Cout[i + (size_t)t * p] = acc;
+  }
+  for (int t = tid; t < nout; t += blockDim.x) lam[t] = sig[order[t]];
+  if (tid == 0) {
+    info[0] = r;
+    info[1] = sw;
+  }
+}
+
+void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* lambda, int* info, cplx* scratch,
+               cudaStream_t st) {
+  const int np = (p + 1) & ~1;
+  size_t smem = (size_t)2 * np * np * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
+    attr = true;
+  }
+  rr_kernel<<<1, RR_THREADS, smem, st>>>(G, p, nb, drop_tol, C, lambda, info, scratch);
+}
+
+// Standalone Hermitian eigensolver (tests): w ascending, V columns in the same order.
+__global__ void __launch_bounds__(RR_THREADS) heevj_kernel(const cplx* __restrict__ Ain, int n, double* w, cplx* Vout,
+                                                           int* info) {
+  extern __shared__ __align__(16) unsigned char rsm[];
+  const int np = (n + 1) & ~1, ld = np;
+  cplx* A = reinterpret_cast<cplx*>(rsm);
+  cplx* V = A + np * np;
+  __shared__ JacSm js;
+  __shared__ double sig[RR_MAXN];
+  __shared__ int order[RR_MAXN];
+  for (int e = threadIdx.x; e < np * np; e += blockDim.x) {
+    int i = e % np, j = e / np;
+    A[e] = (i < n && j < n) ? Ain[i + (size_t)j * n] : mk(0, 0);
+    V[e] = mk(i == j ? 1.0 : 0.0, 0.0);
+  }
+  __syncthreads();
+  int sw = jacobi_smem(A, V, n, np, ld, js, 60);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) sig[i] = A[i + i * ld].x;
+  __syncthreads();
+  rank_sort(sig, n, order);
+  __syncthreads();
+  for (int e = threadIdx.x; e < n * n; e += blockDim.x) {
+    int i = e % n, t = e / n;
+    Vout[i + (size_t)t * n] = V[i + order[t] * ld];
+  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) w[t] = sig[order[t]];
+  if (threadIdx.x == 0) info[0] = sw;
+}
+
+void launch_heevj(const cplx* A, int n, double* w, cplx* V, int* info, cudaStream_t st) {
+  const int np = (n + 1) & ~1;
+  size_t smem = (size_t)2 * np * np * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(heevj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
+    attr = true;
+  }
+  heevj_kernel<<<1, RR_THREADS, smem, st>>>(A, n, w, V, info);
+}

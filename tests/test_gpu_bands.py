@@ -1,0 +1,181 @@
+"""GPU eigenvalue parity: pc_bands (device LOBPCG) against the oracle's eigenvalues and closed forms.
+Bar: relative error <= 1e-8 (BASELINE.json north_star)."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import pc_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+PI = math.pi
+GOLD = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
+TOL = 1e-7   # Res_j tolerance for parity runs (reading R13): eigenvalue error ~ Res^2 / gap
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2511_17107_b200 import api as a
+    return a
+
+
+def golden(name):
+    rows = {}
+    for line in open(os.path.join(GOLD, name)):
+        if line.startswith("#") or not line.strip():
+            continue
+        key, *vals = line.split()
+        rows[key] = np.array([float(v) for v in vals])
+    return rows
+
+
+def rel(a, b):
+    return float(np.max(np.abs(np.asarray(a) - np.asarray(b)) / np.abs(np.asarray(b))))
+
+
+def test_c1_vacuum_n8_golden(api):
+    """BASELINE config 1: SC vacuum n=8, 6 smallest vs closed form."""
+    g = golden("c1_vacuum_n8.txt")
+    ctx = api.pc_create(np.eye(3), 8, np.eye(3), np.zeros((4, 8, 8, 8), np.uint8))
+    r = api.pc_bands(ctx, [[PI, PI, PI], [PI / 7, 3 * PI / 5, 4 * PI / 13]], nev=6, tol=TOL)
+    assert (r["status"] == 0).all()
+    assert rel(r["omega2"][0], g["k_a"]) <= 1e-8
+    assert rel(r["omega2"][1], g["k_b"]) <= 1e-8
+    # preconditioned vacuum operator is the identity: LOBPCG converges at once
+    assert r["iters"].max() <= 3
+
+
+def test_homogeneous_n8_golden(api):
+    g = golden("homog_n8_R.txt")
+    for lat in ("sc", "fcc"):
+        A = synth.lattice(lat)
+        ctx = api.pc_create(A, 8, synth.eps_pseudochiral(), synth.make_masks("full", A, 8))
+        r = api.pc_bands(ctx, [[PI, PI, PI]], nev=10, tol=TOL)
+        assert r["status"][0] == 0
+        assert rel(r["omega2"][0], g[lat]) <= 1e-8
+
+
+@pytest.mark.parametrize("lat,n,k,eps,geo", [
+    ("sc", 6, (PI, PI, PI), "pc", "random"),
+    ("fcc", 6, (0.7, -1.1, 2.0), "pc", "random"),
+    ("sc", 8, (0.0, 0.0, 0.0), "pc", "random"),
+    ("fcc", 8, (PI, PI, PI), "sdd", "random"),
+    ("bcc", 6, (PI, 0, PI), "sdd", "random"),
+    ("sc", 8, (0.2, 0.1, 0.0), "iso", "sphere"),
+])
+def test_bands_match_dense_oracle(api, lat, n, k, eps, geo):
+    A = synth.lattice(lat)
+    e = {"pc": synth.eps_pseudochiral(), "sdd": synth.eps_sdd(), "iso": synth.eps_isotropic(13.0)}[eps]
+    masks = synth.make_masks(geo, A, n, seed=31)
+    ctx = api.pc_create(A, n, e, masks)
+    r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
+    assert r["status"][0] == 0
+    op = O.PenalizedOperator(n, np.array(k), A, e, masks)
+    ref = O.eigs_dense(op, 10)
+    assert rel(r["omega2"][0], ref) <= 1e-8
+    assert (r["resid"][0] <= TOL).all()
+
+
+def test_bands_match_iterative_oracle_fcc_n16(api):
+    """Pseudochiral FCC diamond (the bench's workload shape) at n=16 vs the oracle's SciPy solve."""
+    A = synth.lattice("fcc")
+    n = 16
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("fcc_diamond", A, n)
+    k = np.array([PI, PI, PI])
+    ctx = api.pc_create(A, n, e, masks)
+    r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
+    assert r["status"][0] == 0
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    ref, res = O.eigs_iterative(op, 10, tol=1e-10, seed=3)
+    assert rel(r["omega2"][0], ref) <= 1e-8
+
+
+def _vacuum_closed(n, k, A, nev, gamma):
+    h = 1.0 / n
+    th = 2 * PI * np.arange(n) / n
+    l1 = (1 - np.exp(-1j * th)) / h
+    l0 = (1 + np.exp(-1j * th)) / 2
+    B = np.linalg.inv(A)
+    g1 = [l1[None, None, :], l1[None, :, None], l1[:, None, None]]
+    g0 = [l0[None, None, :], l0[None, :, None], l0[:, None, None]]
+    k2 = 0
+    for i in range(3):
+        k2 = k2 + np.abs(sum(B[j, i] * g1[j] for j in range(3)) + 1j * k[i] * g0[i]) ** 2
+    k2 = np.broadcast_to(k2, (n, n, n)).ravel()
+    vals = np.sort(np.concatenate([k2, k2, gamma * k2]))
+    if not np.any(k):
+        vals = vals[3:]
+    return vals[:nev]
+
+
+@pytest.mark.parametrize("lat,n,k", [("sc", 64, (0.5, 0.0, 0.0)), ("fcc", 128, (PI, PI, PI)), ("sc", 32, (0, 0, 0))])
+def test_bands_vacuum_closed_form_large(api, lat, n, k):
+    """Vacuum at the large sizes: {|kappa|^2 (x2), gamma |kappa|^2}, including
+    the spurious gamma-modes inside the window (reading R11)."""
+    A = synth.lattice(lat)
+    ctx = api.pc_create(A, n, np.eye(3), np.zeros((4, n, n, n), np.uint8))
+    r = api.pc_bands(ctx, [k], nev=10, tol=1e-6)
+    ref = _vacuum_closed(n, np.array(k), A, 10, O.gamma_rule(k))
+    assert rel(r["omega2"][0], ref) <= 1e-8
+
+
+def test_bands_homogeneous_closed_form_n32(api):
+    """Homogeneous pseudochiral FCC at n=32: per-mode 3x3 closed form."""
+    n, A, e = 32, synth.lattice("fcc"), synth.eps_pseudochiral()
+    k = np.array([PI / 2, 2 * PI, PI / 2])
+    h = 1.0 / n
+    th = 2 * PI * np.arange(n) / n
+    l1 = (1 - np.exp(-1j * th)) / h
+    l0 = (1 + np.exp(-1j * th)) / 2
+    B = np.linalg.inv(A)
+    m1, m2, m3 = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    m = [m1.ravel(), m2.ravel(), m3.ravel()]
+    kap = np.stack([sum(B[j, i] * l1[m[j]] for j in range(3)) + 1j * k[i] * l0[m[i]] for i in range(3)], axis=1)
+    KA = np.zeros((kap.shape[0], 3, 3), complex)
+    KA[:, 0, 1], KA[:, 0, 2], KA[:, 1, 0] = -kap[:, 2], kap[:, 1], kap[:, 2]
+    KA[:, 1, 2], KA[:, 2, 0], KA[:, 2, 1] = -kap[:, 0], -kap[:, 1], kap[:, 0]
+    t12 = l0[m[0]] * np.conj(l0[m[1]])
+    Mh = np.broadcast_to(e, (kap.shape[0], 3, 3)).copy()
+    Mh[:, 0, 1] = e[0, 1] * t12
+    Mh[:, 1, 0] = np.conj(e[0, 1]) * np.conj(t12)
+    gamma = O.gamma_rule(k)
+    K = KA @ Mh @ np.conj(np.transpose(KA, (0, 2, 1))) + gamma * np.conj(kap)[:, :, None] * kap[:, None, :]
+    ref = np.sort(np.linalg.eigvalsh(K).ravel())[:10]
+    ctx = api.pc_create(A, n, e, synth.make_masks("full", A, n))
+    r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
+    assert rel(r["omega2"][0], ref) <= 1e-8
+
+
+def test_bands_determinism_and_sharding_seed(api):
+    """Same seed -> bit-identical; results of k-point i do not depend on how the path is split."""
+    A = synth.lattice("sc")
+    n = 8
+    masks = synth.make_masks("random", A, n, seed=2)
+    ctx = api.pc_create(A, n, synth.eps_pseudochiral(), masks)
+    ks = synth.kpath("sc", 2)[:4]
+    r1 = api.pc_bands(ctx, ks, nev=6, tol=1e-8, seed=5)
+    r2 = api.pc_bands(ctx, ks, nev=6, tol=1e-8, seed=5)
+    assert np.array_equal(r1["omega2"], r2["omega2"]) and np.array_equal(r1["iters"], r2["iters"])
+    api.pc_set_option(ctx, "kindex_offset", 2)
+    r3 = api.pc_bands(ctx, ks[2:], nev=6, tol=1e-8, seed=5)
+    assert np.array_equal(r3["omega2"], r1["omega2"][2:])
+
+
+def test_bands_eigenvectors(api):
+    n, A = 8, synth.lattice("fcc")
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("random", A, n, seed=12)
+    ctx = api.pc_create(A, n, e, masks)
+    k = np.array([0.4, 1.0, -0.3])
+    ev = torch.empty(6, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    r = api.pc_bands(ctx, [k], nev=6, tol=1e-9, evecs=ev)
+    V = ev.cpu().numpy()
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    AV = op.apply_fourier(V)
+    res = np.linalg.norm(AV - r["omega2"][0][:, None] * V, axis=1)
+    assert np.allclose(np.linalg.norm(V, axis=1), 1.0, atol=1e-12)
+    assert res.max() <= 1e-8

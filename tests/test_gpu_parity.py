@@ -1,0 +1,210 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle on the same seeded inputs.
+
+Bars (BASELINE.json north_star): operator apply relative error <= 1e-12 per column (2-norm),
+eigenvalues relative error <= 1e-8.  Sub-steps (FFT, M_eps, K_P^{-1}) are held to 1e-13/1e-14.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import pc_oracle as O
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+PI = math.pi
+
+
+@pytest.fixture(scope="module")
+def api():
+    from paper_2511_17107_b200 import api as a
+    return a
+
+
+def to_dev(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).to("cuda")
+
+
+def relerr_cols(got, ref):
+    num = np.linalg.norm(got - ref, axis=-1)
+    den = np.linalg.norm(ref, axis=-1)
+    return float(np.max(num / den))
+
+
+# ------------------------------------------------------------------------------------- FFT
+@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 100, 120, 128])
+def test_fft3_matches_paper_F3(api, n):
+    ctx = api.pc_create(np.eye(3), n, np.eye(3), np.zeros((4, n, n, n), np.uint8))
+    x = synth.random_block(n, 2, seed=n)
+    X = to_dev(x)
+    Y = torch.empty_like(X)
+    api.pc_fft3(ctx, X, Y, api.PC_FFT_TO_FOURIER)
+    ref = np.stack([O.fft3_real_to_fourier(x[c], n) for c in range(2)])
+    assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-13
+    Z = torch.empty_like(X)
+    api.pc_fft3(ctx, Y, Z, api.PC_FFT_TO_REAL)
+    assert relerr_cols(Z.cpu().numpy(), x) <= 1e-13
+
+
+# ------------------------------------------------------------------------------------- M_eps
+@pytest.mark.parametrize("n", [4, 6, 8, 16])
+@pytest.mark.parametrize("eps,mode", [("pc", "crossdof"), ("sdd", "crossdof"), ("ext", "crossdof"),
+                                      ("sdd", "trivial"), ("pc", "trivial"), ("diag", "diagonal")])
+def test_eps_stencil_matches_oracle(api, n, eps, mode):
+    e = {"pc": synth.eps_pseudochiral(), "sdd": synth.eps_sdd(), "ext": synth.eps_extreme(),
+         "diag": np.diag([0.2, 0.5, 0.9]).astype(complex)}[eps]
+    masks = synth.make_masks("random", np.eye(3), n, seed=7 * n)
+    ctx = api.pc_create(np.eye(3), n, e, masks, eps_mode=mode)
+    x = synth.random_block(n, 3, seed=1)
+    Y = torch.empty(3, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    api.pc_apply_eps(ctx, to_dev(x), Y)
+    M = O.permittivity_matrix(e, masks, mode)
+    ref = (M @ x.T).T
+    assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-14
+
+
+# ------------------------------------------------------------------------------------- K_P^{-1}
+@pytest.mark.parametrize("lat,n,k", [("sc", 8, (0.3, -1.1, 2.0)), ("fcc", 12, (PI, PI, PI)), ("sc", 6, (0, 0, 0)),
+                                     ("bcc", 8, (0.05, 0.02, -0.01)), ("fcc", 16, (0, 2 * PI, 0))])
+def test_precond_matches_oracle(api, lat, n, k):
+    A = synth.lattice(lat)
+    ctx = api.pc_create(A, n, np.eye(3), np.zeros((4, n, n, n), np.uint8))
+    r = synth.random_block(n, 2, seed=3)
+    P = torch.empty(2, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    api.pc_precond(ctx, k, to_dev(r), P)
+    gamma = O.gamma_rule(k)
+    assert abs(api.pc_gamma(ctx, k) - gamma) <= 1e-12 * gamma
+    ref = O.precond_fourier(n, np.array(k), A, gamma, r)
+    assert relerr_cols(P.cpu().numpy(), ref) <= 1e-12
+
+
+# ------------------------------------------------------------------------------------- apply
+APPLY_CASES = [
+    ("sc", "random", "pc", "crossdof", 4, (PI, PI, PI)),
+    ("sc", "random", "sdd", "crossdof", 6, (0.3, -1.2, 2.5)),
+    ("fcc", "random", "pc", "crossdof", 8, (0.7, 1.9, -2.2)),
+    ("bcc", "random", "sdd", "crossdof", 8, (2 * PI, 0, 0)),
+    ("sc", "random", "pc", "trivial", 8, (0.1, 0.05, 0.0)),
+    ("fcc", "random", "ext", "crossdof", 10, (0.0, 0.0, 0.0)),
+    ("sc", "sphere", "iso", "crossdof", 16, (PI / 2, 0.0, 0.0)),
+    ("sc", "sc_curv", "pc", "crossdof", 24, (PI, PI, 0)),
+    ("fcc", "fcc_diamond", "pc", "crossdof", 32, (PI, PI, PI)),
+    ("fcc", "fcc_diamond", "pc", "crossdof", 20, (PI / 2, 2 * PI, PI / 2)),
+]
+
+
+def _eps(name):
+    return {"pc": synth.eps_pseudochiral(), "sdd": synth.eps_sdd(), "ext": synth.eps_extreme(),
+            "iso": synth.eps_isotropic(13.0)}[name]
+
+
+@pytest.mark.parametrize("lat,geo,eps,mode,n,k", APPLY_CASES)
+def test_apply_fourier_matches_oracle(api, lat, geo, eps, mode, n, k):
+    A = synth.lattice(lat)
+    e = _eps(eps)
+    masks = synth.make_masks(geo, A, n, seed=11)
+    ctx = api.pc_create(A, n, e, masks, eps_mode=mode)
+    x = np.concatenate([synth.random_block(n, 2, seed=5), synth.random_block(n, 1, seed=6, kind="smooth")])
+    Y = torch.empty(3, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    api.pc_apply(ctx, k, to_dev(x), Y)
+    op = O.PenalizedOperator(n, np.array(k), A, e, masks, mode)
+    ref = op.apply_fourier(x)
+    assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("lat,n,k", [("sc", 8, (0.4, 0.1, -0.3)), ("fcc", 12, (PI, PI, PI))])
+def test_apply_real_space_matches_oracle(api, lat, n, k):
+    A = synth.lattice(lat)
+    e = synth.eps_sdd()
+    masks = synth.make_masks("random", A, n, seed=2)
+    ctx = api.pc_create(A, n, e, masks)
+    H = synth.random_block(n, 2, seed=9)
+    Y = torch.empty(2, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    api.pc_apply(ctx, k, to_dev(H), Y, space=api.PC_SPACE_REAL)
+    op = O.PenalizedOperator(n, np.array(k), A, e, masks)
+    ref = np.stack([op.apply_real(H[c]) for c in range(2)])
+    assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-12
+
+
+def test_apply_gamma_override_and_ld(api):
+    """Strided blocks (ld > 3N^3) and the gamma override path."""
+    n, A, k = 8, synth.lattice("sc"), (0.2, 0.3, 0.1)
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("random", A, n, seed=4)
+    ctx = api.pc_create(A, n, e, masks, gamma_override=2.5)
+    x = synth.random_block(n, 2, seed=8)
+    big = torch.zeros(2, 3 * n ** 3 + 64, dtype=torch.complex128, device="cuda")
+    big[:, : 3 * n ** 3] = to_dev(x)
+    out = torch.zeros_like(big)
+    api.pc_apply(ctx, k, big[:, : 3 * n ** 3], out[:, : 3 * n ** 3])
+    ref = O.PenalizedOperator(n, np.array(k), A, e, masks, gamma=2.5).apply_fourier(x)
+    assert relerr_cols(out[:, : 3 * n ** 3].cpu().numpy(), ref) <= 1e-12
+    assert torch.all(out[:, 3 * n ** 3:] == 0)
+
+
+# ------------------------------------------------------------------- full size (bench config)
+def test_apply_full_size_n128_fcc_pseudochiral(api):
+    """BASELINE config C4 at full size, the bench's launch configuration (a 15-column block)."""
+    W = synth.WORKLOADS["C4"]
+    n, A, e, masks = W.n, W.A(), W.eps1(), W.masks()
+    k = np.array([PI, PI, PI])
+    ctx = api.pc_create(A, n, e, masks)
+    x = np.concatenate([synth.random_block(n, 1, seed=21), synth.random_block(n, 1, seed=22, kind="smooth")])
+    X = torch.zeros(15, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    X[:2] = to_dev(x)
+    X[2:] = torch.randn(13, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    Y = torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y)
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    ref = op.apply_fourier(x)
+    assert relerr_cols(Y[:2].cpu().numpy(), ref) <= 1e-12
+
+
+def _kappa2_closed(n, k, A):
+    """|kappa(m)|^2 from the symbols lambda_1 = (1 - e^{-i theta})/h, lambda_0 = (1 + e^{-i theta})/2."""
+    h = 1.0 / n
+    th = 2 * PI * np.arange(n) / n
+    l1 = (1 - np.exp(-1j * th)) / h
+    l0 = (1 + np.exp(-1j * th)) / 2
+    B = np.linalg.inv(A)
+    grids = [l1[None, None, :], l1[None, :, None], l1[:, None, None]]
+    g0 = [l0[None, None, :], l0[None, :, None], l0[:, None, None]]
+    tot = 0
+    for i in range(3):
+        kap = sum(B[j, i] * grids[j] for j in range(3)) + 1j * k[i] * g0[i]
+        tot = tot + np.abs(kap) ** 2
+    return np.broadcast_to(tot, (n, n, n))
+
+
+@pytest.mark.parametrize("lat,n", [("sc", 128), ("fcc", 128), ("fcc", 192)])
+def test_identity_selftest_full_size(api, lat, n):
+    """M = I, gamma = 1: A_c A_c^H + B^H B = diag(L, L, L), so the apply is
+    multiplication by |kappa(m)|^2 per mode -- an oracle-free check at the full sizes."""
+    A = synth.lattice(lat)
+    k = np.array([0.9, -2.1, PI])
+    ctx = api.pc_create(A, n, np.eye(3), np.zeros((4, n, n, n), np.uint8), gamma_override=1.0)
+    X = torch.randn(2, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    Y = torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y)
+    k2 = torch.from_numpy(np.tile(_kappa2_closed(n, k, A).reshape(-1), 3)).to("cuda")
+    ref = X * k2[None, :]
+    err = (torch.linalg.vector_norm(Y - ref, dim=1) / torch.linalg.vector_norm(ref, dim=1)).max().item()
+    assert err <= 1e-12
+
+
+# ------------------------------------------------------------------------------------- Jacobi
+@pytest.mark.parametrize("n", [1, 2, 5, 16, 45, 75, 80])
+def test_device_jacobi_eigh(api, n):
+    rng = np.random.default_rng(n)
+    M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
+    M = M + M.conj().T
+    # widen the spectrum to mimic H (1 .. 1e7)
+    Q, _ = np.linalg.qr(M)
+    M = Q @ np.diag(np.logspace(0, 7, n)) @ Q.conj().T if n > 3 else M
+    M = 0.5 * (M + M.conj().T)
+    w, V, sw = api.pc_debug_heevj(M)
+    wr = np.linalg.eigvalsh(M)
+    assert np.allclose(w, wr, rtol=1e-12, atol=1e-12 * np.abs(wr).max())
+    assert np.allclose(V.conj().T @ V, np.eye(n), atol=1e-12)
+    assert np.linalg.norm(M @ V - V * w[None, :]) <= 1e-12 * np.linalg.norm(M)
