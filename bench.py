@@ -1,0 +1,393 @@
+#!/usr/bin/env python
+"""Benchmark: k-points/s of the full 10-band pseudochiral band solve at n = 128 (BASELINE.json metric,
+config 4 of BASELINE.json: FCC lattice, diamond inclusion, eps_1 pseudochiral, tol 1e-5 as in
+PAPER.md:1064), plus the pc_apply HBM bandwidth.
+
+    python bench.py [--gpus N --steps K --warmup W]                     # our arm (libpcband.so)
+    python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   # N > 1 (NCCL)
+    python bench.py --impl reference                                    # the CPU oracle arm
+
+A step = one Bloch vector solved to tolerance by pc_bands (symbols, K_A^H/FFT/M_eps/FFT/K_A applies,
+K_P^{-1}, Gram, Rayleigh-Ritz, updates -- every row of SURVEY §8(a)).  Each rank solves K distinct
+k-points of the 49-point path (weak scaling); value = all ranks' k-points / max-over-ranks time.
+One JSON line is printed by rank 0.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "k-points/sec (10 bands, n=128, FP64) and pc_apply HBM GB/s vs 8 TB/s"
+PAPER_ITERS_FCC_PC = 51.3   # mean LOBPCG iterations, pseudochiral FCC, CrossDoF, N=120
+
+
+def load_json(path, default=None):
+    try:
+        with open(path) as f:
+            return json.load(f)
+    except Exception:
+        return default
+
+
+def peaks():
+    mp = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json"), {}) or {}
+    fp = load_json(os.path.join(ROOT, "profiles", "fp64_peaks.json"), {}) or {}
+    hbm = mp.get("hbm_gbs")
+    hbm_src = "MEASURED_PEAKS.json hbm_gbs (measured)"
+    if hbm is None:
+        hbm, hbm_src = 6650.0, "B200_PROFILING.md fallback"
+    fp64 = fp.get("dmma_m8n8k4_tflops")
+    fp64_src = "profiles/fp64_peaks.json (DMMA m8n8k4 microbenchmark, measured on this pool)"
+    if fp64 is None:
+        bf = mp.get("bf16_tflops", 1590.0)
+        fp64, fp64_src = bf * 40.0 / 2250.0, "bf16 measured peak x nominal fp64/bf16 ratio (40/2250)"
+    return hbm, hbm_src, fp64, fp64_src
+
+
+# ------------------------------------------------------------------------------------------
+# clocks sampler (nvidia-smi during the timed region)
+# ------------------------------------------------------------------------------------------
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu):
+        self.gpu = gpu
+        self.proc = None
+        self.f = None
+
+    def start(self):
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", delete=False, suffix=".csv")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "200", "-i", str(self.gpu)], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.strip().split(", ") for r in self.f.read().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            try:
+                sm.append(float(r[1]))
+                smax = float(r[2])
+                for nm, v in zip(names, r[5:9]):
+                    if v.strip().lower() == "active":
+                        reasons.add(nm)
+            except Exception:
+                continue
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------------------------------
+# CPU oracle timing (cpu_baseline and --impl reference)
+# ------------------------------------------------------------------------------------------
+def oracle_sample(W, k, nsample_cols=1, build=None, masks=None):
+    """Time the oracle as it stands on a bounded sample of one k-point solve of workload W:
+    sparse assembly (once per k), nsample_cols operator applies + K_P^{-1} solves, and one
+    Rayleigh-Ritz Gram of the 3b-column block.  Returns the component times."""
+    from oracle import pc_oracle as O
+    import synth
+    t0 = time.perf_counter()
+    if masks is None:
+        masks = W.masks()
+    op = build if build is not None else O.PenalizedOperator(W.n, k, W.A(), W.eps1(), masks)
+    t_asm = time.perf_counter() - t0
+    x = synth.random_block(W.n, nsample_cols, seed=3)
+    t0 = time.perf_counter()
+    y = op.apply_fourier(x)
+    t_apply = (time.perf_counter() - t0) / nsample_cols
+    t0 = time.perf_counter()
+    O.precond_fourier(W.n, k, op.A, op.gamma, y)
+    t_prec = (time.perf_counter() - t0) / nsample_cols
+    b = W.nev + 5
+    # one Gram S^H [S AS] of the 3b-column basis on the full vectors (numpy/BLAS), timed on a slab
+    rows = min(op.dim, 1 << 18)
+    S = np.random.default_rng(0).standard_normal((rows, 3 * b)) + 0j
+    t0 = time.perf_counter()
+    S.conj().T @ np.concatenate([S, S], axis=1)
+    t_gram = (time.perf_counter() - t0) * (op.dim / rows)
+    return op, {"assembly_s": t_asm, "apply_s_per_col": t_apply, "precond_s_per_col": t_prec,
+                "gram_s": t_gram, "block": b}
+
+
+def oracle_kpts_per_s(t, iters):
+    """Model of one oracle k-point solve: assembly + iters x (b applies + b K_P^{-1} + 2 Grams)."""
+    b = t["block"]
+    per_it = b * (t["apply_s_per_col"] + t["precond_s_per_col"]) + 2.0 * t["gram_s"]
+    return 1.0 / (t["assembly_s"] + iters * per_it), per_it
+
+
+def run_reference(args):
+    """--impl reference: the CPU oracle arm (rank 0 only; other ranks exit 0)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    import synth
+    W = synth.WORKLOADS[args.workload]
+    kp = W.kpoints()
+    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
+    masks = W.masks()
+    times = []
+    comps = []
+    for s in range(args.warmup + args.steps):
+        k = kp[s % len(kp)]
+        t0 = time.perf_counter()
+        op, t = oracle_sample(W, k, 1, masks=masks)
+        el = time.perf_counter() - t0
+        if s >= args.warmup:
+            times.append(el)
+            comps.append(t)
+    vals = [oracle_kpts_per_s(t, PAPER_ITERS_FCC_PC)[0] for t in comps]
+    value = float(np.mean(vals))
+    sample = (f"per step: oracle sparse assembly of Op(k) at n={W.n} + 1 Fourier-space apply + 1 K_P^-1 column "
+              f"+ one 3b-column Gram; k-point time modelled as assembly + {PAPER_ITERS_FCC_PC} iterations "
+              f"(PAPER.md:1199) x (b={W.nev + 5} applies + preconditioner solves + 2 Grams)")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "k-points/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(times)),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(W, args),
+            "cpu_baseline": {"value": value, "unit": "k-points/s", "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": "k-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "oracle_components": comps[-1] if comps else None}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(W, args):
+    return {"workload": f"{W.name}: {W.lattice.upper()} lattice, {W.geometry} inclusion, eps1={W.eps} "
+                        f"(pseudochiral eps_lat=13 beta=0.875, PAPER.md:1083-1093), n={W.n}, {W.nev} bands, "
+                        f"tol={args.tol:g}, k-path {len(W.kpoints())} points",
+            "n": W.n, "nev": W.nev, "block": W.nev + 5, "tol": args.tol, "lattice": W.lattice,
+            "geometry": W.geometry, "eps_mode": "crossdof",
+            "l2": "no flush: per-k working set ~15 GB >> 126 MB L2"}
+
+
+# ------------------------------------------------------------------------------------------
+# our arm
+# ------------------------------------------------------------------------------------------
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=4)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C4")
+    ap.add_argument("--tol", type=float, default=1e-5)
+    ap.add_argument("--maxit", type=int, default=500)
+    ap.add_argument("--apply-cols", type=int, default=15)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=2)
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    import torch.distributed as dist
+
+    import synth
+    from paper_2511_17107_b200 import api, bands
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize()
+
+    W = synth.WORKLOADS[args.workload]
+    A, eps1 = W.A(), W.eps1()
+    masks = W.masks()
+    kp = W.kpoints()
+    nk = len(kp)
+    ctx = api.pc_create(A, W.n, eps1, masks, device=local)
+
+    def kidx(s):
+        return (rank + world * s) % nk
+
+    # warm-up: W solves (allocations, first-touch, kernel attribute setup)
+    wit = []
+    for s in range(args.warmup):
+        om, rs, it, st = bands.solve_local(ctx, kp, [kidx(s)], W.nev, args.tol, args.maxit, 0)
+        wit.append(int(it[0]))
+    api.pc_stats(ctx, reset=True)
+    api.pc_set_option(ctx, "profile", 1)
+    clk = Clocks(local)
+    barrier()
+    clk.start()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    res = []
+    for s in range(args.warmup, args.warmup + args.steps):
+        res.append(bands.solve_local(ctx, kp, [kidx(s)], W.nev, args.tol, args.maxit, 0))
+    e1.record()
+    torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1)
+    clocks = clk.stop()
+    barrier()
+    stats = api.pc_stats(ctx)
+    api.pc_set_option(ctx, "profile", 0)
+    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms_max = float(t.item())
+    value = world * args.steps / (ms_max / 1000.0)
+    iters = [int(r[2][0]) for r in res]
+    status = [int(r[3][0]) for r in res]
+    # the one collective of the method: all-gather of eigenvalues
+    idx = [kidx(s) for s in range(args.warmup, args.warmup + args.steps)]
+    om = np.concatenate([r[0] for r in res])
+    rs = np.concatenate([r[1] for r in res])
+    gathered = None
+    if world > 1:
+        loc = torch.from_numpy(np.concatenate([np.array(idx)[:, None], om], axis=1)).to(dev)
+        out = torch.empty((world * loc.shape[0], loc.shape[1]), dtype=loc.dtype, device=dev)
+        dist.all_gather_into_tensor(out, loc)
+        gathered = out.shape[0]
+
+    # ---- pc_apply bandwidth (second half of the metric): a b-column block at n=128
+    ncol = args.apply_cols
+    X = torch.randn(ncol, 3 * W.n ** 3, dtype=torch.complex128, device=dev)
+    Y = torch.empty_like(X)
+    kk = kp[kidx(0)]
+    for _ in range(3):
+        api.pc_apply(ctx, kk, X, Y)
+    api.pc_stats(ctx, reset=True)
+    api.pc_set_option(ctx, "profile", 1)
+    torch.cuda.synchronize()
+    reps = 5
+    a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a0.record()
+    for _ in range(reps):
+        api.pc_apply(ctx, kk, X, Y)
+    a1.record()
+    torch.cuda.synchronize()
+    apply_ms = a0.elapsed_time(a1) / reps
+    astats = api.pc_stats(ctx)
+    api.pc_set_option(ctx, "profile", 0)
+    hbm, hbm_src, fp64, fp64_src = peaks()
+    pts = W.n ** 3 * ncol
+    alg_gbs = 336.0 * pts / (apply_ms * 1e6)
+    design_gbs = 720.0 * pts / (apply_ms * 1e6)
+    apply = {"cols": ncol, "ms": apply_ms, "alg_bytes_per_point_col": 336,
+             "alg_gbs": alg_gbs, "frac_of_8tbs": alg_gbs / 8000.0, "frac_of_measured_hbm": alg_gbs / hbm,
+             "design_bytes_per_point_col": 720, "design_gbs": design_gbs,
+             "kernels": {k: {"ms_per_apply": v["ms"] / reps, "gbs": (v["bytes"] / v["ms"] / 1e6) if v["ms"] else None}
+                         for k, v in astats.items() if isinstance(v, dict) and v["count"]}}
+    del X, Y
+
+    # ---- roofline of the dominant kernel class in the timed region
+    cls = {k: v for k, v in stats.items() if isinstance(v, dict) and v["ms"] > 0}
+    dom = max(cls, key=lambda k: cls[k]["ms"])
+    d = cls[dom]
+    traffic = load_json(os.path.join(ROOT, "profiles", "traffic.json"), {}) or {}
+    if dom in ("gram", "update", "rr"):
+        ach = d["flops"] / (d["ms"] * 1e9)
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": fp64, "unit": "TFLOP/s",
+                "frac": ach / fp64, "peak_source": fp64_src, "dtype": "fp64 (DMMA m8n8k4)"}
+    else:
+        ach = d["bytes"] / (d["ms"] * 1e6)
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
+                "peak_source": hbm_src}
+    roof["traffic"] = traffic.get(dom)
+    roof["share_of_step"] = d["ms"] / ms
+    roof["avg_launch_group_ms"] = d["ms"] / max(1, d["count"])
+
+    # ---- end to end through the public API with host buffers (rank-local)
+    e2e = None
+    if args.e2e_steps > 0:
+        pin = torch.from_numpy(masks.reshape(-1)).pin_memory()
+        pinned_masks = pin.numpy().reshape(masks.shape)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        e_it = []
+        for s in range(args.e2e_steps):
+            c2 = api.pc_create(A, W.n, eps1, pinned_masks, device=local)
+            api.pc_set_option(c2, "kindex_offset", kidx(s))
+            r = api.pc_bands(c2, kp[kidx(s):kidx(s) + 1], nev=W.nev, tol=args.tol, maxit=args.maxit)
+            e_it.append(int(r["iters"][0]))
+            c2.close()
+        torch.cuda.synchronize()
+        te = time.perf_counter() - t0
+        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        b = W.nev + 5
+        h2d = W.n ** 3 + 16 * W.n + 24 + 4 * W.n ** 3 * 0
+        d2h = int(np.mean(e_it)) * (2 * b * 8 + 8) + b * 8
+        e2e = {"value": world * args.e2e_steps / float(tt.item()), "unit": "k-points/s",
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "note": "per step: pc_create from pinned host masks (packed I1/I2/I3/IV upload, device "
+                       "allocation) + pc_bands(k) with host k-point and host omega^2/Res outputs + pc_destroy"}
+
+    # ---- CPU oracle baseline (rank 0, N = 1 only)
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        try:
+            cores = len(os.sched_getaffinity(0))
+            _, tcomp = oracle_sample(W, kk, 1, masks=masks)
+            v, per_it = oracle_kpts_per_s(tcomp, float(np.mean(iters)))
+            cpu = {"value": v, "unit": "k-points/s", "cores": cores, "kind": "oracle",
+                   "sample": f"oracle sparse assembly at n={W.n} + 1 apply + 1 K_P^-1 column + one 3b-column Gram "
+                             f"timed; k-point modelled as assembly + {np.mean(iters):.1f} iterations (this run's "
+                             f"GPU mean) x (b={W.nev + 5} applies+precond + 2 Grams) = "
+                             f"{tcomp['assembly_s']:.1f} s + {np.mean(iters):.1f} x {per_it:.1f} s",
+                   "components": tcomp}
+        except Exception as ex:  # pragma: no cover
+            cpu = {"value": None, "error": str(ex)}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": "k-points/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+                "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                "config": workload_config(W, args) | {"kpoints_per_rank": args.steps,
+                                                      "parallelism": f"k-path sharded over {world} GPU(s)"},
+                "iters": iters, "status": status, "warmup_iters": wit,
+                "omega2_first_k": om[0].tolist(), "resid_max": float(rs.max()),
+                "apply": apply, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": stats["launches"], "clocks": clocks,
+                "kernel_classes": {k: {"ms": v["ms"], "share": v["ms"] / ms,
+                                       "tflops": v["flops"] / (v["ms"] * 1e9) if v["ms"] else None,
+                                       "gbs": v["bytes"] / (v["ms"] * 1e6) if v["ms"] else None}
+                                   for k, v in cls.items()},
+                "gathered_rows": gathered}
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

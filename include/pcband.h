@@ -168,9 +168,11 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
 int pc_set_option(pc_ctx *ctx, const char *key, double value);
 
 /*
- * pc_stats — cumulative per-kernel-class launch counts and CUDA-event durations (ms) since the
- * last reset, recorded when option "profile" = 1.  out: host, 2*PC_NSTAT doubles laid out
- * [count_0, ms_0, count_1, ms_1, ...] in the order of enum pc_stat.  reset != 0 clears them.
+ * pc_stats — cumulative per-kernel-class statistics since the last reset.  out: host,
+ * 4*PC_NSTAT + 1 doubles: for class i (enum order below) out[4i] = timed launch groups,
+ * out[4i+1] = CUDA-event milliseconds on the launching stream (only while option "profile" = 1),
+ * out[4i+2] = algorithmic flops, out[4i+3] = algorithmic bytes (what the method must move, not
+ * what the kernels moved); out[4*PC_NSTAT] = number of kernel launches.  reset != 0 clears them.
  */
 enum {
   PC_STAT_FFT_Z_KAH = 0,   /* first inverse pass with K_A^H fused      */

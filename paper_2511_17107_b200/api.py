@@ -207,9 +207,13 @@ def pc_set_option(ctx: Ctx, key: str, value: float):
 
 
 def pc_stats(ctx: Ctx, reset=False):
-    out = np.zeros(2 * len(STAT_NAMES))
+    """Per kernel class: timed groups, CUDA-event ms, algorithmic flops and bytes; plus total launches."""
+    out = np.zeros(4 * len(STAT_NAMES) + 1)
     _check(lib().pc_stats(ctx.h, _dptr(out), 1 if reset else 0))
-    return {nm: {"count": int(out[2 * i]), "ms": float(out[2 * i + 1])} for i, nm in enumerate(STAT_NAMES)}
+    st = {nm: {"count": int(out[4 * i]), "ms": float(out[4 * i + 1]), "flops": float(out[4 * i + 2]),
+               "bytes": float(out[4 * i + 3])} for i, nm in enumerate(STAT_NAMES)}
+    st["launches"] = int(out[-1])
+    return st
 
 
 def pc_debug_heevj(A):

@@ -92,6 +92,9 @@ struct pc_ctx {
   int profile = 0;
   double stat_ms[PC_NSTAT] = {0};
   double stat_cnt[PC_NSTAT] = {0};
+  double stat_flops[PC_NSTAT] = {0};
+  double stat_bytes[PC_NSTAT] = {0};
+  double launches = 0;
   std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> pending;
   std::vector<cudaEvent_t> ev_pool;
 };
@@ -107,12 +110,18 @@ static cudaEvent_t ev_get(pc_ctx* c) {
   cudaEventCreate(&e);
   return e;
 }
+// Times one kernel class (CUDA events on the launching stream) and books its algorithmic work:
+// nl kernel launches, flops and bytes that the method requires for this launch group.
 struct Prof {
   pc_ctx* c;
   int stat;
   cudaStream_t st;
   cudaEvent_t e0 = nullptr;
-  Prof(pc_ctx* c_, int s_, cudaStream_t st_) : c(c_), stat(s_), st(st_) {
+  Prof(pc_ctx* c_, int s_, cudaStream_t st_, int nl = 1, double flops = 0.0, double bytes = 0.0)
+      : c(c_), stat(s_), st(st_) {
+    c->launches += nl;
+    c->stat_flops[s_] += flops;
+    c->stat_bytes[s_] += bytes;
     if (c->profile) {
       e0 = ev_get(c);
       cudaEventRecord(e0, st);
@@ -354,13 +363,19 @@ extern "C" int pc_stats(pc_ctx* c, double* out, int reset) {
   if (!c) return set_err(PC_EINVAL, "pc_stats: null ctx");
   cudaSetDevice(c->device);
   prof_flush(c);
-  if (out)
+  if (out) {
     for (int i = 0; i < PC_NSTAT; i++) {
-      out[2 * i] = c->stat_cnt[i];
-      out[2 * i + 1] = c->stat_ms[i];
+      out[4 * i] = c->stat_cnt[i];
+      out[4 * i + 1] = c->stat_ms[i];
+      out[4 * i + 2] = c->stat_flops[i];
+      out[4 * i + 3] = c->stat_bytes[i];
     }
-  if (reset)
-    for (int i = 0; i < PC_NSTAT; i++) c->stat_cnt[i] = c->stat_ms[i] = 0;
+    out[4 * PC_NSTAT] = c->launches;
+  }
+  if (reset) {
+    for (int i = 0; i < PC_NSTAT; i++) c->stat_cnt[i] = c->stat_ms[i] = c->stat_flops[i] = c->stat_bytes[i] = 0;
+    c->launches = 0;
+  }
   return PC_OK;
 }
 
@@ -373,6 +388,7 @@ static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
   Sym3 s;
   std::memcpy(s.B, c->B, sizeof(s.B));
   for (int i = 0; i < 3; i++) s.k[i] = k[i];
+  c->launches += 1;
   launch_ktab(c->d_ktab, c->d_tw, c->n, s, st);
   // |kappa|^2 <= 1e-28 max|kappa|^2 -> pass-through (reading R7); max bounded via the 1-D pieces
   double bound = 0;
@@ -414,26 +430,30 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   const int n = c->n;
   const double inv_n3 = 1.0 / ((double)n * n * n);
   ColPtrs Yc = to_const(Y, nc), Wc = to_const(WS, nc), none{};
+  // algorithmic work per pass: one read + one write of the 3-component field (96 B per point per
+  // column; the last pass also reads x_hat: 144 B), 5 log2(N) flops per point per component
+  const double pts = (double)c->n3 * nc;
+  const double fl = 15.0 * std::log2((double)n) * pts;
   {
-    Prof p(c, PC_STAT_FFT_Z_KAH, st);
+    Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 30.0 * pts, 96.0 * pts);
     CHK(fft_pass(c, 2, +1, 1, X, Y, none, nc, inv_n3, st));
   }
   {
-    Prof p(c, PC_STAT_FFT_MID, st);
+    Prof p(c, PC_STAT_FFT_MID, st, 2, 2 * fl, 2 * 96.0 * pts);
     CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
     CHK(fft_pass(c, 0, +1, 0, Yc, Y, none, nc, 1.0, st));
   }
   {
-    Prof p(c, PC_STAT_EPS, st);
+    Prof p(c, PC_STAT_EPS, st, 1, 100.0 * pts, 97.0 * pts);
     launch_eps(c->eps_mode, Yc, WS, nc, n, c->d_mask, c->ec, st);
   }
   {
-    Prof p(c, PC_STAT_FFT_MID, st);
+    Prof p(c, PC_STAT_FFT_MID, st, 2, 2 * fl, 2 * 96.0 * pts);
     CHK(fft_pass(c, 0, -1, 0, Wc, WS, none, nc, 1.0, st));
     CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
   }
   {
-    Prof p(c, PC_STAT_FFT_Z_KA, st);
+    Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 40.0 * pts, 144.0 * pts);
     CHK(fft_pass(c, 2, -1, 2, Wc, Y, X, nc, 1.0, st));
   }
   return PC_OK;
@@ -443,7 +463,8 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
 static int fft3(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, int nc, int dir, cudaStream_t st) {
   const double s = 1.0 / std::sqrt((double)c->n);
   ColPtrs Yc = to_const(Y, nc), none{};
-  Prof p(c, PC_STAT_FFT_MID, st);
+  const double pts = (double)c->n3 * nc;
+  Prof p(c, PC_STAT_FFT_MID, st, 3, 3 * 15.0 * std::log2((double)c->n) * pts, 3 * 96.0 * pts);
   CHK(fft_pass(c, 0, dir, 0, X, Y, none, nc, s, st));
   CHK(fft_pass(c, 1, dir, 0, Yc, Y, none, nc, s, st));
   CHK(fft_pass(c, 2, dir, 0, Yc, Y, none, nc, s, st));
@@ -541,7 +562,7 @@ extern "C" int pc_precond(pc_ctx* c, const double k[3], const void* R, void* P, 
     MutColPtrs p;
     block_ptrs(R, ld, j0, nc, r);
     block_ptrs(P, ld, j0, nc, p);
-    Prof pf(c, PC_STAT_RESID, st);
+    Prof pf(c, PC_STAT_RESID, st, 1, 60.0 * c->n3 * nc, 96.0 * c->n3 * nc);
     launch_precond(r, p, nc, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, st);
   }
   CU(cudaGetLastError());
@@ -559,7 +580,7 @@ extern "C" int pc_apply_eps(pc_ctx* c, const void* E, void* Y, int ncols, long l
     MutColPtrs y;
     block_ptrs(E, ld, j0, nc, e);
     block_ptrs(Y, ld, j0, nc, y);
-    Prof pf(c, PC_STAT_EPS, st);
+    Prof pf(c, PC_STAT_EPS, st, 1, 100.0 * c->n3 * nc, 97.0 * c->n3 * nc);
     launch_eps(c->eps_mode, e, y, nc, c->n, c->d_mask, c->ec, st);
   }
   CU(cudaGetLastError());
@@ -694,7 +715,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   };
   auto rr = [&](int p) -> int {
     {
-      Prof pf(c, PC_STAT_RR, st);
+      Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
       launch_rr(dG, p, b, c->drop_tol, dC, dLam, dInfo, dScr, st);
     }
     cudaMemcpyAsync(hInfo, dInfo, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
@@ -705,7 +726,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
 
   // ---- start block X0 (counter-based Gaussian), AX0, Rayleigh-Ritz on span(X0)
   {
-    Prof pf(c, PC_STAT_OTHER, st);
+    Prof pf(c, PC_STAT_OTHER, st, 1, 0.0, 16.0 * len * b);
     MutColPtrs x0;
     mcols(sX, all, x0, 0);
     launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)kidx), deflate ? (int)c->n3 : 0, st);
@@ -716,13 +737,13 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     ccols(sX, all, S, 0);
     ccols(sX, all, T, 0);
     ccols(sAX, all, T, b);
-    Prof pf(c, PC_STAT_GRAM, st);
+    Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * b * 2 * b, 16.0 * len * 2 * b);
     launch_gram(S, b, T, 2 * b, len, dG, c->gpart.as<cplx>(), st);
   }
   int rank = rr(b);
   if (rank < b) return set_err(PC_ENUMERIC, "pc_bands: start block is rank deficient");
   {
-    Prof pf(c, PC_STAT_UPDATE, st);
+    Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * b * b, 2 * 16.0 * len * 2 * b);
     ColPtrs S;
     MutColPtrs Y;
     ccols(sX, all, S, 0);
@@ -742,7 +763,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   for (;; it++) {
     // residuals, K_P^{-1} R for every column
     {
-      Prof pf(c, PC_STAT_RESID, st);
+      Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 3.0 * 16.0 * len * b);
       ColPtrs X, AX;
       MutColPtrs W;
       ccols(sX, all, X, 0);
@@ -786,7 +807,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       ccols(AWW, act, T, p + b);
       if (haveP) ccols(sAP, act, T, p + b + na);
       {
-        Prof pf(c, PC_STAT_GRAM, st);
+        Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * p * 2 * p, 16.0 * len * 2 * p);
         launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
       }
       rank = rr(p);
@@ -798,7 +819,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     }
     // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images
     {
-      Prof pf(c, PC_STAT_UPDATE, st);
+      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b, 2 * 16.0 * len * (p + 2 * b));
       ColPtrs S;
       MutColPtrs Y1, Y2;
       ccols(sX, all, S, 0);
@@ -829,6 +850,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       X.p[j] = col(sX, j);
       Y.p[j] = evec_out + (size_t)j * len;
     }
+    c->launches += 1;
     normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, st>>>(X, dNorm, Y, len);
   }
   CU(cudaStreamSynchronize(st));
