@@ -164,6 +164,15 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "drop_tol"     Rayleigh-Ritz rank threshold on the scaled Gram eigenvalues (default 1e-12)
  *   "kindex_offset" global index of kpts[0] in pc_bands (start-block seeds are keyed by it, so
  *                  results do not depend on how a k-path is split across GPUs; default 0)
+ *   "start"        0: Gaussian start block; 1 (default): transverse plane waves of the b/2 modes
+ *                  with the smallest |kappa|^2 (eigenvectors of K_P) plus a seeded Gaussian admixture
+ *   "start_noise"  relative size of that admixture (default 1e-3)
+ *   "sticky_lock"  1: a locked column stays locked; 0 (default): it re-enters the search block if
+ *                  its residual rises above tol again
+ *   "gram_refresh" every n-th iteration forms the full Gram matrices instead of using
+ *                  X^H X = I, X^H A X = Lambda (default 16; 0 = never)
+ *   "p_restart"    1 (default): drop the P block when the basis is numerically rank deficient
+ *   "verbose"      1: per-iteration residuals on stderr
  */
 int pc_set_option(pc_ctx *ctx, const char *key, double value);
 

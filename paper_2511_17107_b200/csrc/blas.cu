@@ -25,55 +25,67 @@ DEV void cp_async16_zfill(void* smem, const void* gmem, bool valid) {
 
 // ------------------------------------------------------------------------------------------
 // Gram: partial[split][n][m] = sum over the split's rows of conj(S[r][m]) T[r][n]
-// CTA output block 48 x 48 (complex), 6 warps as 2 (m) x 3 (n), warp tile 24 x 16 = 3 x 2 m8n8.
+// CTA output block BM x BN (complex) = (WARPS_M * WM * 8) x (WARPS_N * WN * 8); each warp owns
+// WM x WN m8n8 tiles (real and imaginary accumulators).  Rows stream through a 2-stage cp.async
+// pipeline in chunks of G_KC complex rows; the split-K partials are reduced in a fixed order.
 // ------------------------------------------------------------------------------------------
-constexpr int G_BM = 48, G_BN = 48, G_KC = 32, G_PITCH = 2 * G_KC + 4, G_THREADS = 192;
-constexpr size_t G_SMEM = 2 * (size_t)(G_BM + G_BN) * G_PITCH * sizeof(double);
+constexpr int G_KC = 32, G_PITCH = 2 * G_KC + 4;
 
-__global__ void __launch_bounds__(G_THREADS) gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len,
-                                                         long long rows_per_split, int nmb, cplx* partial) {
+template <int WM, int WN, int WARPS_M, int WARPS_N>
+struct GramCfg {
+  static constexpr int BM = WARPS_M * WM * 8, BN = WARPS_N * WN * 8;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr size_t SMEM = 2 * (size_t)(BM + BN) * G_PITCH * sizeof(double);
+};
+
+template <int WM, int WN, int WARPS_M, int WARPS_N>
+__global__ void __launch_bounds__(GramCfg<WM, WN, WARPS_M, WARPS_N>::THREADS)
+gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_per_split, int nmb, cplx* partial) {
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, NTH = Cfg::THREADS;
   extern __shared__ __align__(16) double gsm[];
-  double* As = gsm;                                // [2][G_BM][G_PITCH]
-  double* Bs = gsm + 2 * G_BM * G_PITCH;           // [2][G_BN][G_PITCH]
+  double* As = gsm;                       // [2][BM][G_PITCH]
+  double* Bs = gsm + 2 * BM * G_PITCH;    // [2][BN][G_PITCH]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % 2, wn = warp / 2;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
   const int mb = blockIdx.x % nmb, nb = blockIdx.x / nmb;
-  const int m0 = mb * G_BM, n0 = nb * G_BN;
+  const int m0 = mb * BM, n0 = nb * BN;
   const long long r0 = (long long)blockIdx.y * rows_per_split;
   const long long r1 = min(len, r0 + rows_per_split);
 
-  double accR[3][2][2], accI[3][2][2];
+  double accR[WM][WN][2], accI[WM][WN][2];
 #pragma unroll
-  for (int i = 0; i < 3; i++)
+  for (int i = 0; i < WM; i++)
 #pragma unroll
-    for (int j = 0; j < 2; j++) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
+    for (int j = 0; j < WN; j++) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
 
   const cplx* dummy = S.p[0];
   auto load_chunk = [&](int stage, long long rbase) {
-    // (G_BM + G_BN) columns x G_KC complex rows
-    for (int e = tid; e < (G_BM + G_BN) * G_KC; e += G_THREADS) {
+    for (int e = tid; e < (BM + BN) * G_KC; e += NTH) {
       int c = e / G_KC, r = e % G_KC;
       long long row = rbase + r;
       bool okr = row < r1;
       double* dst;
       const cplx* src = dummy;
       bool ok;
-      if (c < G_BM) {
+      if (c < BM) {
         int m = m0 + c;
         ok = okr && m < p;
         if (ok) src = S.p[m] + row;
-        dst = As + (stage * G_BM + c) * G_PITCH + 2 * r;
+        dst = As + (stage * BM + c) * G_PITCH + 2 * r;
       } else {
-        int n = n0 + (c - G_BM);
+        int n = n0 + (c - BM);
         ok = okr && n < q;
         if (ok) src = T.p[n] + row;
-        dst = Bs + (stage * G_BN + (c - G_BM)) * G_PITCH + 2 * r;
+        dst = Bs + (stage * BN + (c - BM)) * G_PITCH + 2 * r;
       }
       cp_async16_zfill(dst, src, ok);
     }
     cp_async_commit();
   };
 
+  // warp tiles entirely outside [0, p) x [0, q) skip their MMAs (warp-uniform)
+  const bool live = (m0 + wm * WM * 8 < p) && (n0 + wn * WN * 8 < q);
   const int nchunks = (r1 > r0) ? (int)((r1 - r0 + G_KC - 1) / G_KC) : 0;
   if (nchunks > 0) load_chunk(0, r0);
   for (int ch = 0; ch < nchunks; ch++) {
@@ -85,40 +97,42 @@ __global__ void __launch_bounds__(G_THREADS) gram_kernel(ColPtrs S, int p, ColPt
       cp_async_wait<0>();
     }
     __syncthreads();
-    const double* A = As + st * G_BM * G_PITCH;
-    const double* B = Bs + st * G_BN * G_PITCH;
+    if (live) {
+      const double* A = As + st * BM * G_PITCH;
+      const double* B = Bs + st * BN * G_PITCH;
 #pragma unroll 4
-    for (int s4 = 0; s4 < 2 * G_KC / 4; s4++) {
-      const int kk = 4 * s4 + (lane & 3);
-      double a[3], b[2], bi[2];
+      for (int s4 = 0; s4 < 2 * G_KC / 4; s4++) {
+        const int kk = 4 * s4 + (lane & 3);
+        double a[WM], b[WN], bi[WN];
 #pragma unroll
-      for (int mt = 0; mt < 3; mt++) a[mt] = A[(wm * 24 + mt * 8 + (lane >> 2)) * G_PITCH + kk];
+        for (int mt = 0; mt < WM; mt++) a[mt] = A[(wm * WM * 8 + mt * 8 + (lane >> 2)) * G_PITCH + kk];
 #pragma unroll
-      for (int nt = 0; nt < 2; nt++) {
-        b[nt] = B[(wn * 16 + nt * 8 + (lane >> 2)) * G_PITCH + kk];
-        double bx = __shfl_xor_sync(0xffffffffu, b[nt], 1);
-        bi[nt] = (lane & 1) ? -bx : bx;
-      }
-#pragma unroll
-      for (int mt = 0; mt < 3; mt++)
-#pragma unroll
-        for (int nt = 0; nt < 2; nt++) {
-          dmma(accR[mt][nt][0], accR[mt][nt][1], a[mt], b[nt]);
-          dmma(accI[mt][nt][0], accI[mt][nt][1], a[mt], bi[nt]);
+        for (int nt = 0; nt < WN; nt++) {
+          b[nt] = B[(wn * WN * 8 + nt * 8 + (lane >> 2)) * G_PITCH + kk];
+          double bx = __shfl_xor_sync(0xffffffffu, b[nt], 1);
+          bi[nt] = (lane & 1) ? -bx : bx;
         }
+#pragma unroll
+        for (int mt = 0; mt < WM; mt++)
+#pragma unroll
+          for (int nt = 0; nt < WN; nt++) {
+            dmma(accR[mt][nt][0], accR[mt][nt][1], a[mt], b[nt]);
+            dmma(accI[mt][nt][0], accI[mt][nt][1], a[mt], bi[nt]);
+          }
+      }
     }
     __syncthreads();
   }
 
   cplx* out = partial + (size_t)blockIdx.y * p * q;
 #pragma unroll
-  for (int mt = 0; mt < 3; mt++)
+  for (int mt = 0; mt < WM; mt++)
 #pragma unroll
-    for (int nt = 0; nt < 2; nt++)
+    for (int nt = 0; nt < WN; nt++)
 #pragma unroll
       for (int e = 0; e < 2; e++) {
-        int m = m0 + wm * 24 + mt * 8 + (lane >> 2);
-        int n = n0 + wn * 16 + nt * 8 + 2 * (lane & 3) + e;
+        int m = m0 + wm * WM * 8 + mt * 8 + (lane >> 2);
+        int n = n0 + wn * WN * 8 + nt * 8 + 2 * (lane & 3) + e;
         if (m < p && n < q) out[(size_t)n * p + m] = mk(accR[mt][nt][e], accI[mt][nt][e]);
       }
 }
@@ -131,95 +145,149 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
   G[idx] = acc;
 }
 
-static int gram_nsplit(int p, int q, long long len) {
-  int nblk = ((p + G_BM - 1) / G_BM) * ((q + G_BN - 1) / G_BN);
-  int ns = std::max(1, (2 * 148 + nblk - 1) / nblk);
-  long long maxs = (len + 4 * G_KC - 1) / (4 * G_KC);  // at least 4 chunks per split
-  return (int)std::max(1LL, std::min<long long>(ns, maxs));
-}
-
 size_t gram_partial_bytes(int p, int q) { return (size_t)2 * 148 * p * q * sizeof(cplx) + 4096; }
 
-void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
-                 cudaStream_t st) {
+template <int WM, int WN, int WARPS_M, int WARPS_N>
+static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
+                     int ctas_per_sm, cudaStream_t st) {
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N>;
+  auto kern = gram_kernel<WM, WN, WARPS_M, WARPS_N>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G_SMEM);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     attr = true;
   }
-  int nmb = (p + G_BM - 1) / G_BM, nnb = (q + G_BN - 1) / G_BN;
-  int ns = gram_nsplit(p, q, len);
+  const int nmb = (p + Cfg::BM - 1) / Cfg::BM, nnb = (q + Cfg::BN - 1) / Cfg::BN;
+  const int nblk = nmb * nnb;
+  int ns = std::max(1, (ctas_per_sm * 148 + nblk - 1) / nblk);
+  ns = (int)std::max(1LL, std::min<long long>(ns, (len + 4 * G_KC - 1) / (4 * G_KC)));
   long long rps = (len + ns - 1) / ns;
   rps = (rps + G_KC - 1) / G_KC * G_KC;
   ns = (int)((len + rps - 1) / rps);
-  gram_kernel<<<dim3(nmb * nnb, ns), G_THREADS, G_SMEM, st>>>(S, p, T, q, len, rps, nmb, partial);
-  int pq = p * q;
+  kern<<<dim3(nblk, ns), Cfg::THREADS, Cfg::SMEM, st>>>(S, p, T, q, len, rps, nmb, partial);
+  const int pq = p * q;
   gram_reduce_kernel<<<(pq + 255) / 256, 256, 0, st>>>(partial, ns, pq, G);
+}
+
+// Choose the CTA output block with the least padded area (ties: fewer blocks).
+void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
+                 cudaStream_t st) {
+  struct Opt { int bm, bn; };
+  const Opt opts[4] = {{48, 64}, {48, 48}, {32, 64}, {16, 32}};
+  int best = 0;
+  double best_cost = 1e300;
+  for (int i = 0; i < 4; i++) {
+    double area = (double)((p + opts[i].bm - 1) / opts[i].bm * opts[i].bm) * ((q + opts[i].bn - 1) / opts[i].bn * opts[i].bn);
+    double cost = area * (1.0 + 0.02 * i);
+    if (cost < best_cost) { best_cost = cost; best = i; }
+  }
+  switch (best) {
+    case 0: run_gram<3, 2, 2, 4>(S, p, T, q, len, G, partial, 1, st); break;
+    case 1: run_gram<3, 2, 2, 3>(S, p, T, q, len, G, partial, 2, st); break;
+    case 2: run_gram<2, 2, 2, 4>(S, p, T, q, len, G, partial, 2, st); break;
+    default: run_gram<2, 2, 1, 2>(S, p, T, q, len, G, partial, 4, st); break;
+  }
+}
+
+// [G_M | G_A] (p x 2p) for S = [X (b) | W (nw) | P (np)] from Gp = S^H [W P AW AP] (p x 2c, c = nw+np),
+// using X^H X = I and X^H A X = diag(lambda) (X are the current Ritz vectors) and Hermitian symmetry.
+__global__ void gram_assemble_kernel(const cplx* __restrict__ Gp, const double* __restrict__ lam, int b, int c,
+                                     cplx* G) {
+  const int p = b + c;
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= 2 * p * p) return;
+  const int half = idx / (p * p), e = idx % (p * p);
+  const int i = e % p, j = e / p;
+  cplx v;
+  if (i < b && j < b) {
+    v = (i == j) ? mk(half ? lam[i] : 1.0, 0.0) : mk(0, 0);
+  } else if (j >= b) {
+    v = Gp[(size_t)(half * c + (j - b)) * p + i];
+  } else {  // i >= b, j < b: conj of (j, i)
+    v = conjg(Gp[(size_t)(half * c + (i - b)) * p + j]);
+  }
+  G[(size_t)half * p * p + e] = v;
+}
+
+void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st) {
+  const int p = b + c;
+  gram_assemble_kernel<<<(2 * p * p + 255) / 256, 256, 0, st>>>(Gp, lam, b, c, G);
 }
 
 // ------------------------------------------------------------------------------------------
 // Update: phase 1  acc = sum_{m in [split, p)} S[:, m] C[m, :]  -> Y1 (optional)
 //         phase 2  acc += sum_{m in [0, split)} S[:, m] C[m, :] -> Y2 (+ Add)
-// r <= 32 output columns (4 n-tiles of 8), CTA = 8 warps x 8 rows = 64 rows, persistent over row tiles.
-// S tile in smem as [row][m] complex with pitch PS = 2 mod 8 (conflict-free fragments); C as [c][m].
+// r <= 8 NT output columns.  CTA = 8 warps x 8 rows = 64-row tiles, persistent over row tiles with a
+// 2-stage cp.async pipeline (tile t+1 streams in while tile t is multiplied).  S tile in smem as
+// [row][m] complex with pitch PS = 2 mod 8 (conflict-free fragments); C as [c][m], same pitch.
 // ------------------------------------------------------------------------------------------
 constexpr int U_ROWS = 64, U_THREADS = 256;
 
-DEV int pitch2mod8(int p) {
+HD int pitch2mod8(int p) {
   int x = p + 1;
   while ((x & 7) != 2) x++;
   return x;
 }
 
+template <int NT>
 __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, const cplx* __restrict__ C, int ldc,
                                                            int r, int split, MutColPtrs Y1, int has_y1, MutColPtrs Y2,
                                                            ColPtrs Add, int has_add, long long len) {
   extern __shared__ __align__(16) double usm[];
   const int pe = (p + 1) & ~1;  // even number of S columns (k' multiple of 4)
   const int PS = pitch2mod8(pe);
-  const int PC = pitch2mod8(pe);
-  cplx* Ss = reinterpret_cast<cplx*>(usm);   // [U_ROWS][PS]
-  cplx* Cs = Ss + U_ROWS * PS;               // [32][PC]
+  cplx* Ss = reinterpret_cast<cplx*>(usm);   // [2][U_ROWS][PS]
+  cplx* Cs = Ss + 2 * U_ROWS * PS;           // [NT*8][PS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
 
-  // C -> smem (zero padded to 32 columns x pe rows)
-  for (int e = tid; e < 32 * pe; e += U_THREADS) {
+  for (int e = tid; e < NT * 8 * pe; e += U_THREADS) {
     int c = e / pe, m = e % pe;
-    Cs[c * PC + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
+    Cs[c * PS + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
   }
   const long long ntiles = (len + U_ROWS - 1) / U_ROWS;
   const cplx* dummy = S.p[0];
-  for (long long t = blockIdx.x; t < ntiles; t += gridDim.x) {
+  auto load_tile = [&](int stage, long long t) {
     const long long rbase = t * U_ROWS;
-    __syncthreads();  // previous tile's smem reads done (and C staged on the first pass)
+    cplx* dst = Ss + stage * U_ROWS * PS;
     for (int e = tid; e < U_ROWS * pe; e += U_THREADS) {
       int m = e / U_ROWS, rr = e % U_ROWS;
       long long row = rbase + rr;
       bool ok = (m < p) && (row < len);
-      cp_async16_zfill(&Ss[rr * PS + m], ok ? (const void*)(S.p[m] + row) : (const void*)dummy, ok);
+      cp_async16_zfill(&dst[rr * PS + m], ok ? (const void*)(S.p[m] + row) : (const void*)dummy, ok);
     }
     cp_async_commit();
-    cp_async_wait<0>();
+  };
+  long long t = blockIdx.x;
+  if (t < ntiles) load_tile(0, t);
+  for (int i = 0; t < ntiles; t += gridDim.x, i++) {
+    const int st = i & 1;
+    if (t + gridDim.x < ntiles) {
+      load_tile(st ^ 1, t + gridDim.x);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
     __syncthreads();
-
-    double accR[4][2], accI[4][2];
+    const long long rbase = t * U_ROWS;
+    double accR[NT][2], accI[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < 4; nt++) accR[nt][0] = accR[nt][1] = accI[nt][0] = accI[nt][1] = 0.0;
-    const double* Sd = reinterpret_cast<const double*>(Ss);
+    for (int nt = 0; nt < NT; nt++) accR[nt][0] = accR[nt][1] = accI[nt][0] = accI[nt][1] = 0.0;
+    const double* Sd = reinterpret_cast<const double*>(Ss + st * U_ROWS * PS);
     const int arow = warp * 8 + (lane >> 2);
 
     auto kloop = [&](int mlo, int mhi) {  // contributions of S columns m in [mlo, mhi)
+#pragma unroll 2
       for (int m2 = mlo & ~1; m2 < mhi; m2 += 2) {  // one k4 step = 2 complex m
         const int kk = 2 * m2 + (lane & 3);
-        double a = Sd[arow * 2 * PS + kk];
+        const double a = Sd[arow * 2 * PS + kk];
         const int mm = m2 + ((lane & 3) >> 1);
         const bool in = (mm >= mlo) && (mm < mhi);
 #pragma unroll
-        for (int nt = 0; nt < 4; nt++) {
-          cplx cv = Cs[(nt * 8 + (lane >> 2)) * PC + mm];
+        for (int nt = 0; nt < NT; nt++) {
+          cplx cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
           if (!in) cv = mk(0, 0);
-          double br = (lane & 1) ? -cv.y : cv.x;
-          double bi = (lane & 1) ? cv.x : cv.y;
+          const double br = (lane & 1) ? -cv.y : cv.x;
+          const double bi = (lane & 1) ? cv.x : cv.y;
           dmma(accR[nt][0], accR[nt][1], a, br);
           dmma(accI[nt][0], accI[nt][1], a, bi);
         }
@@ -229,7 +297,7 @@ __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, con
       long long row = rbase + warp * 8 + (lane >> 2);
       if (row >= len) return;
 #pragma unroll
-      for (int nt = 0; nt < 4; nt++)
+      for (int nt = 0; nt < NT; nt++)
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           int c = nt * 8 + 2 * (lane & 3) + e;
@@ -244,24 +312,32 @@ __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, con
     if (has_y1) store(Y1, false);
     kloop(0, split);
     store(Y2, has_add != 0);
+    __syncthreads();  // stage st is refilled by the next iteration's prefetch
   }
+}
+
+template <int NT>
+static void run_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
+                       const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
+  const int pe = (p + 1) & ~1, ps = pitch2mod8(pe);
+  const size_t smem = (size_t)(2 * U_ROWS * ps + NT * 8 * ps) * sizeof(cplx);
+  static bool attr = false;
+  if (!attr) {
+    cudaFuncSetAttribute(update_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    attr = true;
+  }
+  const long long ntiles = (len + U_ROWS - 1) / U_ROWS;
+  const int occ = std::max(1, std::min(3, (int)((227 * 1024) / (smem + 1024))));
+  const int grid = (int)std::min<long long>(ntiles, 148LL * occ);
+  MutColPtrs y1 = Y1 ? *Y1 : MutColPtrs{};
+  ColPtrs ad = add ? *add : ColPtrs{};
+  update_kernel<NT><<<grid, U_THREADS, smem, st>>>(S, p, C, ldc, r, split, y1, Y1 ? 1 : 0, Y2, ad, add ? 1 : 0, len);
 }
 
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
-  int pe = (p + 1) & ~1;
-  int ps = pe + 1;
-  while ((ps & 7) != 2) ps++;
-  size_t smem = (size_t)(U_ROWS * ps + 32 * ps) * sizeof(cplx);
-  static int attr_bytes = 0;
-  if ((int)smem > attr_bytes) {
-    cudaFuncSetAttribute(update_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr_bytes = 200 * 1024;
-  }
-  long long ntiles = (len + U_ROWS - 1) / U_ROWS;
-  int occ = smem <= 70 * 1024 ? 3 : (smem <= 110 * 1024 ? 2 : 1);
-  int grid = (int)std::min<long long>(ntiles, 148LL * occ);
-  MutColPtrs y1 = Y1 ? *Y1 : MutColPtrs{};
-  ColPtrs ad = add ? *add : ColPtrs{};
-  update_kernel<<<grid, U_THREADS, smem, st>>>(S, p, C, ldc, r, split, y1, Y1 ? 1 : 0, Y2, ad, add ? 1 : 0, len);
+  if (r <= 8) run_update<1>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else if (r <= 16) run_update<2>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else if (r <= 24) run_update<3>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else run_update<4>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
 }

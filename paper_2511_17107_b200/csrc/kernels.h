@@ -49,11 +49,23 @@ void launch_resid(const ColPtrs& X, const ColPtrs& AX, const MutColPtrs& W, cons
                   const cplx* kt, double gamma, double thr, int deflate0, double* partial, double* norms,
                   cudaStream_t st);
 void launch_randn(const MutColPtrs& X, int ncols, long long len, unsigned long long seed, int deflate_stride,
-                  cudaStream_t st);
+                  double scale, cudaStream_t st);
+// plane-wave start block: per-CTA PW_T smallest |kappa|^2 (pw_grid() CTAs), then a host-built scatter
+#define PW_T 16
+struct PwEntry {
+  int col, mode;
+  double v[6];  // 3 complex components
+};
+int pw_grid();
+void launch_kappa2_topk(const cplx* kt, int n, double thr, double* outv, int* outi, cudaStream_t st);
+void launch_pw_scatter(const MutColPtrs& X, const PwEntry* e, int ne, int n3, cudaStream_t st);
 
 // dense block algebra ------------------------------------------------------------------------
 // G (p x q, column-major, ld p) = S^H T over rows [0, len): S p columns, T q columns.
 size_t gram_partial_bytes(int p, int q);
+// [G_M | G_A] (p x 2p) from Gp = S^H [W P AW AP] (p x 2c), S = [X W P], b = |X|, c = |W| + |P|,
+// assuming X^H X = I, X^H A X = diag(lambda) (Ritz vectors of the previous Rayleigh-Ritz step).
+void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                  cudaStream_t st);
 // Block update (r <= 32 output columns, C column-major ld = ldc):

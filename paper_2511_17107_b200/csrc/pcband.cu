@@ -64,6 +64,10 @@ struct DevBuf {
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
 
+// pinned host staging: [0, 2048) norms, [2048, 2056) info ints, [PIN_PWV..) top-k |kappa|^2,
+// [PIN_PWI..) top-k mode ints, [PIN_PWE..) plane-wave scatter entries
+enum { PIN_PWV = 4096, PIN_PWI = 4096 + 5120, PIN_PWE = 4096 + 5120 + 2560, PIN_DOUBLES = 16384 };
+
 struct pc_ctx {
   int n = 0, device = 0, eps_mode = 1;
   long long n3 = 0, len = 0;  // N^3, 3 N^3
@@ -84,6 +88,11 @@ struct pc_ctx {
   long long kindex_offset = 0;  // global index of kpts[0] (seeds independent of sharding)
   int verbose = 0;
   int p_restart = 1;  // drop the P block when the Rayleigh-Ritz basis is rank deficient
+  int sticky_lock = 0;         // 1: locked columns stay locked (SciPy's activeMask &=); 0: may re-activate
+  int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
+  int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
+  double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
+  DevBuf pwbuf;
   // LOBPCG storage
   DevBuf lob, small, gpart;
   double* h_pinned = nullptr;
@@ -304,7 +313,8 @@ extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double ep
   if (cudaMalloc(&c->d_ktab, 9 * n * sizeof(cplx)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: ktab alloc");
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(PC_ECUDA, "pc_create: stream");
-  if (cudaMallocHost(&c->h_pinned, 4096 * sizeof(double)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: pinned");
+  if (cudaMallocHost(&c->h_pinned, PIN_DOUBLES * sizeof(double)) != cudaSuccess)
+    return fail(PC_ENOMEM, "pc_create: pinned");
   *out = c;
   return PC_OK;
 }
@@ -322,6 +332,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   c->lob.release();
   c->small.release();
   c->gpart.release();
+  c->pwbuf.release();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->stream) cudaStreamDestroy(c->stream);
   delete c;
@@ -355,6 +366,10 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "kindex_offset") c->kindex_offset = (long long)v;
   else if (k == "verbose") c->verbose = (int)v;
   else if (k == "p_restart") c->p_restart = (int)v;
+  else if (k == "start") c->start_mode = (int)v;
+  else if (k == "sticky_lock") c->sticky_lock = (int)v;
+  else if (k == "gram_refresh") c->gram_refresh = (int)v;
+  else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
 }
@@ -653,6 +668,67 @@ __global__ void normalize_copy_kernel(ColPtrs X, const double* norms, MutColPtrs
     Y.p[j][i] = s * X.p[j][i];
 }
 
+// Adds unit transverse plane waves to the b start columns: modes in ascending |kappa|^2 (ties by
+// index), two polarisations u with kappa^T u = 0 (so K_B u = 0) per mode.
+static int plane_wave_start(pc_ctx* c, const MutColPtrs& x0, int b, cudaStream_t st) {
+  const int G = pw_grid(), n = c->n;
+  CHK(c->pwbuf.ensure((size_t)G * PW_T * (sizeof(double) + sizeof(int)) + 64 * sizeof(PwEntry) +
+                      9 * n * sizeof(cplx) + 256));
+  double* dv = c->pwbuf.as<double>();
+  int* di = reinterpret_cast<int*>(dv + G * PW_T);
+  PwEntry* de = reinterpret_cast<PwEntry*>(di + G * PW_T + 8);
+  launch_kappa2_topk(c->d_ktab, n, c->cur_thr, dv, di, st);
+  double* hv = c->h_pinned + PIN_PWV;
+  int* hi = reinterpret_cast<int*>(c->h_pinned + PIN_PWI);
+  PwEntry* he = reinterpret_cast<PwEntry*>(c->h_pinned + PIN_PWE);
+  std::vector<cplx> kt(9 * n);
+  cudaMemcpyAsync(hv, dv, G * PW_T * sizeof(double), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(hi, di, G * PW_T * sizeof(int), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(kt.data(), c->d_ktab, 9 * n * sizeof(cplx), cudaMemcpyDeviceToHost, st);
+  CU(cudaStreamSynchronize(st));
+  std::vector<std::pair<double, int>> cand;
+  for (int t = 0; t < G * PW_T; t++)
+    if (hi[t] >= 0) cand.push_back({hv[t], hi[t]});
+  std::sort(cand.begin(), cand.end());
+  int ne = 0;
+  for (size_t q = 0; q < cand.size() && ne < b; q++) {
+    const int m = cand[q].second;
+    const int m1 = m % n, m2 = (m / n) % n, m3 = m / (n * n);
+    cplx kap[3];
+    for (int i = 0; i < 3; i++)
+      kap[i] = kt[(3 * i) * n + m1] + kt[(3 * i + 1) * n + m2] + kt[(3 * i + 2) * n + m3];
+    // a = conj(kappa)/|kappa|;  u1 = e - a (a^H e) for the unit axis least aligned with a;  u2 = conj(a x u1)
+    double kn = std::sqrt(abs2(kap[0]) + abs2(kap[1]) + abs2(kap[2]));
+    cplx a[3] = {conjg(kap[0]), conjg(kap[1]), conjg(kap[2])};
+    for (int i = 0; i < 3; i++) a[i] = (1.0 / kn) * a[i];
+    int ax = 0;
+    for (int i = 1; i < 3; i++)
+      if (abs2(a[i]) < abs2(a[ax])) ax = i;
+    cplx u1[3] = {mk(0, 0), mk(0, 0), mk(0, 0)};
+    u1[ax] = mk(1, 0);
+    cplx ahe = conjg(a[ax]);  // a^H e
+    for (int i = 0; i < 3; i++) u1[i] = u1[i] - cmul(a[i], ahe);
+    double u1n = std::sqrt(abs2(u1[0]) + abs2(u1[1]) + abs2(u1[2]));
+    for (int i = 0; i < 3; i++) u1[i] = (1.0 / u1n) * u1[i];
+    cplx u2[3] = {conjg(cmul(a[1], u1[2]) - cmul(a[2], u1[1])), conjg(cmul(a[2], u1[0]) - cmul(a[0], u1[2])),
+                  conjg(cmul(a[0], u1[1]) - cmul(a[1], u1[0]))};
+    double u2n = std::sqrt(abs2(u2[0]) + abs2(u2[1]) + abs2(u2[2]));
+    for (int i = 0; i < 3; i++) u2[i] = (1.0 / u2n) * u2[i];
+    const cplx* us[2] = {u1, u2};
+    for (int pol = 0; pol < 2 && ne < b; pol++, ne++) {
+      he[ne].col = ne;
+      he[ne].mode = m;
+      for (int i = 0; i < 3; i++) {
+        he[ne].v[2 * i] = us[pol][i].x;
+        he[ne].v[2 * i + 1] = us[pol][i].y;
+      }
+    }
+  }
+  cudaMemcpyAsync(de, he, ne * sizeof(PwEntry), cudaMemcpyHostToDevice, st);
+  launch_pw_scatter(x0, de, ne, (int)c->n3, st);
+  return PC_OK;
+}
+
 static unsigned long long mix64(unsigned long long x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -678,13 +754,14 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   enum { XA = 0, AXA, XB, AXB, PA, APA, PB, APB, WW, AWW };
   int sX = XA, sAX = AXA, sXn = XB, sAXn = AXB, sP = PA, sAP = APA, sPn = PB, sAPn = APB;
   // small device buffers: G (maxp x 2maxp), C (maxp x b), lam, info, rr scratch, resid partials, norms
-  const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)2 * maxp * 80;
+  const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)3 * 80 * 80;
   const int rg = resid_grid(c->n);
-  size_t small_bytes = (nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) + 64;
+  size_t small_bytes = (2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) + 64;
   CHK(c->small.ensure(small_bytes));
   CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
   cplx* dG = c->small.as<cplx>();
-  cplx* dC = dG + nG;
+  cplx* dGp = dG + nG;
+  cplx* dC = dGp + nG;
   cplx* dScr = dC + nC;
   double* dLam = reinterpret_cast<double*>(dScr + nScr);
   double* dNorm = dLam + b;
@@ -718,18 +795,26 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
       launch_rr(dG, p, b, c->drop_tol, dC, dLam, dInfo, dScr, st);
     }
-    cudaMemcpyAsync(hInfo, dInfo, 2 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hInfo, dInfo, 3 * sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("rayleigh-ritz: ") + cudaGetErrorString(e));
     return hInfo[0];  // rank
   };
 
-  // ---- start block X0 (counter-based Gaussian), AX0, Rayleigh-Ritz on span(X0)
+  // ---- start block X0, AX0, Rayleigh-Ritz on span(X0).
+  // start 0: counter-based Gaussian columns.  start 1 (default): transverse plane waves of the
+  // b/2 Fourier modes with the smallest |kappa(m)|^2 -- the eigenvectors of K_P, i.e.
+  // of the vacuum operator -- plus a small seeded Gaussian admixture (reading R14: the paper does
+  // not state its start block).
   {
-    Prof pf(c, PC_STAT_OTHER, st, 1, 0.0, 16.0 * len * b);
+    const bool pw = c->start_mode == 1;
+    const double noise = pw ? c->start_noise / std::sqrt((double)len) : 1.0;
+    Prof pf(c, PC_STAT_OTHER, st, pw ? 3 : 1, 0.0, 16.0 * len * b);
     MutColPtrs x0;
     mcols(sX, all, x0, 0);
-    launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)kidx), deflate ? (int)c->n3 : 0, st);
+    launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)kidx), deflate ? (int)c->n3 : 0,
+                 noise, st);
+    if (pw) CHK(plane_wave_start(c, x0, b, st));
   }
   CHK(apply_list(sX, sAX, all));
   {
@@ -780,11 +865,14 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     conv = 1;
     for (int j = 0; j < b; j++) {
       res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
-      if (!(res[j] > tol)) active[j] = 0;  // soft locking: once converged, stays locked
+      // soft locking: a converged column leaves the search block (no W, P); with sticky_lock = 0 it
+      // re-enters if its residual rises above tol again
+      if (!(res[j] > tol)) active[j] = 0;
+      else if (!c->sticky_lock) active[j] = 1;
       if (j < nev && res[j] > tol) conv = 0;
     }
     if (c->verbose) {
-      fprintf(stderr, "[pcband] k%d it %d rank %d res:", kidx, it, rank);
+      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d res:", kidx, it, rank, hInfo[2], hInfo[1]);
       for (int j = 0; j < b; j++) fprintf(stderr, " %.2e%s", res[j], active[j] ? "" : "*");
       fprintf(stderr, "\n");
     }
@@ -798,17 +886,28 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     int p = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
       p = b + na + (haveP ? na : 0);
+      const int cw = p - b;  // |W| + |P|
       ColPtrs S, T;
       ccols(sX, all, S, 0);
       ccols(WW, act, S, b);
       if (haveP) ccols(sP, act, S, b + na);
-      for (int t = 0; t < p; t++) T.p[t] = S.p[t];
-      ccols(sAX, all, T, p);
-      ccols(AWW, act, T, p + b);
-      if (haveP) ccols(sAP, act, T, p + b + na);
-      {
+      const bool full = c->gram_refresh > 0 && (it % c->gram_refresh) == c->gram_refresh - 1;
+      if (full) {  // periodic full Gram S^H [S AS]: no assumption on X (guards against drift)
+        for (int t = 0; t < p; t++) T.p[t] = S.p[t];
+        ccols(sAX, all, T, p);
+        ccols(AWW, act, T, p + b);
+        if (haveP) ccols(sAP, act, T, p + b + na);
         Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * p * 2 * p, 16.0 * len * 2 * p);
         launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
+      } else {
+        // only the blocks that are not known: S^H [W P AW AP]; X^H X = I and X^H A X = Lambda hold for
+        // the Ritz vectors X of the previous step, the rest follows by Hermitian symmetry
+        for (int t = 0; t < cw; t++) T.p[t] = S.p[b + t];
+        ccols(AWW, act, T, cw);
+        if (haveP) ccols(sAP, act, T, cw + na);
+        Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * cw, 16.0 * len * (p + cw));
+        launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st);
+        launch_gram_assemble(dGp, dLam, b, cw, dG, st);
       }
       rank = rr(p);
       if (rank >= p || (rank >= b && !c->p_restart)) break;

@@ -286,7 +286,7 @@ DEV unsigned long long splitmix64(unsigned long long x) {
   return x ^ (x >> 31);
 }
 
-__global__ void randn_kernel(MutColPtrs X, long long len, unsigned long long seed, int deflate_stride) {
+__global__ void randn_kernel(MutColPtrs X, long long len, unsigned long long seed, int deflate_stride, double scale) {
   const int j = blockIdx.y;
   cplx* x = X.p[j];
   for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < len; i += (long long)gridDim.x * blockDim.x) {
@@ -297,13 +297,102 @@ __global__ void randn_kernel(MutColPtrs X, long long len, unsigned long long see
     double r = sqrt(-2.0 * log(u1));
     double sn, cs;
     sincospi(2.0 * u2, &sn, &cs);
-    cplx v = mk(r * cs, r * sn);
+    cplx v = mk(scale * r * cs, scale * r * sn);
     if (deflate_stride > 0 && (i % deflate_stride) == 0) v = mk(0, 0);  // zero Fourier mode 0
     x[i] = v;
   }
 }
 
 void launch_randn(const MutColPtrs& X, int ncols, long long len, unsigned long long seed, int deflate_stride,
-                  cudaStream_t st) {
-  randn_kernel<<<dim3(148 * 4, ncols), 256, 0, st>>>(X, len, seed, deflate_stride);
+                  double scale, cudaStream_t st) {
+  randn_kernel<<<dim3(148 * 4, ncols), 256, 0, st>>>(X, len, seed, deflate_stride, scale);
+}
+
+// ------------------------------------------------------------------------------------------
+// Plane-wave start block support: the PW_T smallest |kappa(m)|^2 per CTA (the low-lying modes of
+// K_P = K_A K_A^H + gamma K_B, whose transverse plane waves are the vacuum
+// eigenvectors).  Modes with |kappa|^2 <= thr (the k = 0 null mode) are skipped.
+// ------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) kappa2_topk_kernel(const cplx* __restrict__ kt, int n, double thr,
+                                                          double* outv, int* outi) {
+  const int n3 = n * n * n;
+  double v[PW_T];
+  int id[PW_T];
+#pragma unroll
+  for (int t = 0; t < PW_T; t++) { v[t] = 1e300; id[t] = -1; }
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < n3; idx += gridDim.x * blockDim.x) {
+    int m1 = idx % n, m2 = (idx / n) % n, m3 = idx / (n * n);
+    cplx k1, k2, k3;
+    kappa_at(kt, n, m1, m2, m3, k1, k2, k3);
+    double q = abs2(k1) + abs2(k2) + abs2(k3);
+    if (q <= thr || !(q < v[PW_T - 1])) continue;
+    // insertion into the sorted list (fully unrolled: registers, no local memory)
+    double cv = q;
+    int ci = idx;
+#pragma unroll
+    for (int t = 0; t < PW_T; t++) {
+      if (cv < v[t]) {
+        double tv = v[t]; int ti = id[t];
+        v[t] = cv; id[t] = ci;
+        cv = tv; ci = ti;
+      }
+    }
+  }
+  // block merge: PW_T rounds of argmin over the thread list heads
+  __shared__ double sv[256];
+  __shared__ int st[256];
+  int head = 0;
+  for (int r = 0; r < PW_T; r++) {
+    double hv = 1e300;
+#pragma unroll
+    for (int t = 0; t < PW_T; t++)
+      if (t == head) hv = v[t];
+    sv[threadIdx.x] = hv;
+    st[threadIdx.x] = threadIdx.x;
+    __syncthreads();
+    for (int s = 128; s > 0; s >>= 1) {
+      if (threadIdx.x < s) {
+        double a = sv[threadIdx.x], b = sv[threadIdx.x + s];
+        if (b < a || (b == a && st[threadIdx.x + s] < st[threadIdx.x])) {
+          sv[threadIdx.x] = b;
+          st[threadIdx.x] = st[threadIdx.x + s];
+        }
+      }
+      __syncthreads();
+    }
+    const int win = st[0];
+    const double wv = sv[0];
+    if (threadIdx.x == win) {
+      int wid = -1;
+#pragma unroll
+      for (int t = 0; t < PW_T; t++)
+        if (t == head) wid = id[t];
+      outv[blockIdx.x * PW_T + r] = wv;
+      outi[blockIdx.x * PW_T + r] = wid;
+      head++;
+    }
+    __syncthreads();
+  }
+}
+
+int pw_grid() { return 148 * 2; }
+
+void launch_kappa2_topk(const cplx* kt, int n, double thr, double* outv, int* outi, cudaStream_t st) {
+  kappa2_topk_kernel<<<pw_grid(), 256, 0, st>>>(kt, n, thr, outv, outi);
+}
+
+// X[col][c * N^3 + mode] += val  for a short host-built list (plane-wave start vectors)
+__global__ void pw_scatter_kernel(MutColPtrs X, const PwEntry* __restrict__ e, int ne, int n3) {
+  int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= ne) return;
+  PwEntry q = e[t];
+  cplx* x = X.p[q.col];
+  for (int c = 0; c < 3; c++) {
+    cplx v = x[(long long)c * n3 + q.mode];
+    x[(long long)c * n3 + q.mode] = mk(v.x + q.v[2 * c], v.y + q.v[2 * c + 1]);
+  }
+}
+
+void launch_pw_scatter(const MutColPtrs& X, const PwEntry* e, int ne, int n3, cudaStream_t st) {
+  if (ne > 0) pw_scatter_kernel<<<(ne + 127) / 128, 128, 0, st>>>(X, e, ne, n3);
 }

@@ -1,11 +1,11 @@
 // On-device Rayleigh-Ritz for LOBPCG: one CTA solves the small projected
 // generalized Hermitian eigenproblem  G_A c = theta G_M c  (p <= RR_MAXN) by
 //   1. symmetric scaling D = diag(G_M)^{-1/2};
-//   2. Jacobi eigendecomposition D G_M D = V Sigma V^H, dropping directions with
-//      sigma < drop_tol * sigma_max (rank-revealing, SVQB-style);
-//   3. T = D V_r Sigma_r^{-1/2}, H = T^H G_A T;
-//   4. Jacobi eigendecomposition H = Q Theta Q^H, ascending;
-//   5. C = T Q[:, :nb], lambda = Theta[:nb].
+//   2a. Cholesky D G_M D = L L^H (all pivots > drop_tol), H = L^{-1} D G_A D L^{-H}, T = D L^{-H};
+//   2b. otherwise (rank-deficient basis): Jacobi D G_M D = V Sigma V^H, drop sigma < drop_tol
+//       sigma_max (SVQB-style), T = D V_r Sigma_r^{-1/2}, H = T^H G_A T;
+//   3. Jacobi eigendecomposition H = Q Theta Q^H, ascending;
+//   4. C = T Q[:, :nb], lambda = Theta[:nb].
 // Cyclic parallel Jacobi with a round-robin (tournament) pairing: per round np/2 disjoint complex
 // rotations U = [[c, s e], [-s conj(e), c]] (e = a_pq/|a_pq|) are applied as 2x2 blocks
 // U_i^H A_{ii'} U_{i'} (one barrier per round) and accumulated into V.
@@ -107,6 +107,35 @@ DEV void rank_sort(const double* w, int n, int* order) {
   }
 }
 
+// In-place Cholesky of the Hermitian n x n matrix in A (column-major, ld): lower triangle <- L with
+// A = L L^H.  Returns false (uniformly across the CTA) when a pivot is <= tau.
+DEV bool cholesky_smem(cplx* A, int n, int ld, double tau, int* flag) {
+  const int tid = threadIdx.x;
+  if (tid == 0) *flag = 1;
+  __syncthreads();
+  for (int j = 0; j < n; j++) {
+    const double piv = A[j + j * ld].x;
+    if (!(piv > tau)) {  // every thread sees the same pivot
+      if (tid == 0) *flag = 0;
+      __syncthreads();
+      return false;
+    }
+    const double d = sqrt(piv);
+    const double inv = 1.0 / d;
+    for (int i = j + 1 + tid; i < n; i += blockDim.x) A[i + j * ld] = inv * A[i + j * ld];
+    __syncthreads();
+    if (tid == 0) A[j + j * ld] = mk(d, 0.0);
+    // trailing update of the lower triangle: A[i][k] -= L[i][j] conj(L[k][j]), j < k <= i
+    const int m = n - j - 1;
+    for (int e = tid; e < m * m; e += blockDim.x) {
+      const int i = j + 1 + e % m, k = j + 1 + e / m;
+      if (k <= i) A[i + k * ld] = A[i + k * ld] - cmul(A[i + j * ld], conjg(A[k + j * ld]));
+    }
+    __syncthreads();
+  }
+  return true;
+}
+
 __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__ G, int p, int nb, double drop_tol,
                                                         cplx* Cout, double* lam, int* info, cplx* scratch) {
   extern __shared__ __align__(16) unsigned char rsm[];
@@ -116,12 +145,15 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   __shared__ JacSm js;
   __shared__ double dsc[RR_MAXN], sig[RR_MAXN];
   __shared__ int keep[RR_MAXN], order[RR_MAXN];
-  __shared__ int rank_sh;
+  __shared__ int rank_sh, chol_flag;
   const int tid = threadIdx.x;
   const cplx* GM = G;
   const cplx* GA = G + (size_t)p * p;
+  cplx* T = scratch;                                   // p x RR_MAXN
+  cplx* U = scratch + (size_t)p * RR_MAXN;             // p x RR_MAXN
+  cplx* Lg = scratch + (size_t)2 * p * RR_MAXN;        // p x p (Cholesky factor copy)
 
-  // 1. scaling
+  // 1. scaling D = diag(G_M)^{-1/2}
   for (int i = tid; i < p; i += blockDim.x) {
     double d = GM[i + (size_t)i * p].x;
     dsc[i] = d > 0.0 ? 1.0 / sqrt(d) : 0.0;
@@ -133,84 +165,158 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
     if (i < p && j < p) v = (dsc[i] * dsc[j]) * GM[i + (size_t)j * p];
     if (i == j && i < p) v.y = 0.0;
     A[e] = v;
-    V[e] = mk(i == j ? 1.0 : 0.0, 0.0);
   }
   __syncthreads();
-  // 2. eig of scaled G_M
-  jacobi_smem(A, V, p, np, ld, js, 40);
-  for (int i = tid; i < p; i += blockDim.x) sig[i] = A[i + i * ld].x;
-  __syncthreads();
-  if (tid == 0) {
-    double smax = 0.0;
-    for (int i = 0; i < p; i++) smax = fmax(smax, sig[i]);
-    int r = 0;
-    for (int i = 0; i < p; i++)
-      if (sig[i] > drop_tol * smax) keep[r++] = i;
-    rank_sh = r;
-  }
-  __syncthreads();
-  const int r = rank_sh;
-  // 3. T = D V_r Sigma_r^{-1/2}  -> scratch T (p x r, ld p)
-  cplx* T = scratch;
-  cplx* U = scratch + (size_t)p * RR_MAXN;
-  for (int e = tid; e < p * r; e += blockDim.x) {
-    int i = e % p, t = e / p;
-    int kk = keep[t];
-    T[i + (size_t)t * p] = (dsc[i] / sqrt(sig[kk])) * V[i + kk * ld];
-  }
-  __syncthreads();
-  // U = G_A T (p x r)
-  for (int e = tid; e < p * r; e += blockDim.x) {
-    int i = e % p, t = e / p;
-    cplx acc = mk(0, 0);
-    for (int j = 0; j < p; j++) acc = cfma(GA[i + (size_t)j * p], T[j + (size_t)t * p], acc);
-    U[i + (size_t)t * p] = acc;
-  }
-  __syncthreads();
-  // H = T^H U (r x r) -> A (padded to rp), V = I
-  const int rp = (r + 1) & ~1;
-  for (int e = tid; e < rp * rp; e += blockDim.x) {
-    int i = e % rp, j = e / rp;
-    cplx v = mk(0, 0);
-    if (i < r && j < r) {
-      for (int k = 0; k < p; k++) v = v + cmulc(T[k + (size_t)i * p], U[k + (size_t)j * p]);
+
+  // 2a. fast path: Cholesky D G_M D = L L^H (pivots above drop_tol), H = L^{-1} D G_A D L^{-H}
+  const bool chol = cholesky_smem(A, p, ld, drop_tol, &chol_flag);
+  int r = p;
+  int rp = np;
+  if (chol) {
+    // Z = L^{-1} (D G_A D) by forward substitution, row by row, into V (smem, ld)
+    for (int i = 0; i < p; i++) {
+      const double inv = 1.0 / A[i + i * ld].x;
+      for (int j = tid; j < p; j += blockDim.x) {
+        cplx acc = (dsc[i] * dsc[j]) * GA[i + (size_t)j * p];
+        for (int k = 0; k < i; k++) acc = acc - cmul(A[i + k * ld], V[k + j * ld]);
+        V[i + j * ld] = inv * acc;
+      }
+      __syncthreads();
     }
-    A[i + j * rp] = v;
-    V[i + j * rp] = mk(i == j ? 1.0 : 0.0, 0.0);
-  }
-  __syncthreads();
-  // Hermitian symmetrisation (rounding): A <- (A + A^H)/2
-  for (int e = tid; e < r * r; e += blockDim.x) {
-    int i = e % r, j = e / r;
-    if (i < j) {
-      cplx a = A[i + j * rp], b = A[j + i * rp];
-      cplx m = mk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
-      A[i + j * rp] = m;
-      A[j + i * rp] = conjg(m);
-    } else if (i == j) {
-      A[i + i * rp].y = 0.0;
+    // H = Z L^{-H} in place, column by column: H[:, j] = (Z[:, j] - sum_{k<j} H[:, k] conj(L[j][k])) / L[j][j]
+    for (int j = 0; j < p; j++) {
+      const double inv = 1.0 / A[j + j * ld].x;
+      for (int i = tid; i < p; i += blockDim.x) {
+        cplx acc = V[i + j * ld];
+        for (int k = 0; k < j; k++) acc = acc - cmul(V[i + k * ld], conjg(A[j + k * ld]));
+        V[i + j * ld] = inv * acc;
+      }
+      __syncthreads();
     }
+    // keep L (global), A <- Hermitian part of H, V <- I
+    for (int e = tid; e < p * p; e += blockDim.x) {
+      int i = e % p, j = e / p;
+      Lg[e] = (i >= j) ? A[i + j * ld] : mk(0, 0);
+    }
+    __syncthreads();
+    for (int e = tid; e < np * np; e += blockDim.x) {
+      int i = e % np, j = e / np;
+      cplx v = mk(0, 0);
+      if (i < p && j < p) {
+        cplx a = V[i + j * ld], b = V[j + i * ld];
+        v = mk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+      }
+      A[i + j * ld] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < np * np; e += blockDim.x) {
+      int i = e % np, j = e / np;
+      V[i + j * ld] = mk(i == j ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+  } else {
+    // 2b. robust path (rank deficient basis): Jacobi on D G_M D, drop sigma < drop_tol sigma_max
+    for (int e = tid; e < np * np; e += blockDim.x) {
+      int i = e % np, j = e / np;
+      cplx v = mk(0, 0);
+      if (i < p && j < p) v = (dsc[i] * dsc[j]) * GM[i + (size_t)j * p];
+      if (i == j && i < p) v.y = 0.0;
+      A[e] = v;
+      V[e] = mk(i == j ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    jacobi_smem(A, V, p, np, ld, js, 40);
+    for (int i = tid; i < p; i += blockDim.x) sig[i] = A[i + i * ld].x;
+    __syncthreads();
+    if (tid == 0) {
+      double smax = 0.0;
+      for (int i = 0; i < p; i++) smax = fmax(smax, sig[i]);
+      int rr = 0;
+      for (int i = 0; i < p; i++)
+        if (sig[i] > drop_tol * smax) keep[rr++] = i;
+      rank_sh = rr;
+    }
+    __syncthreads();
+    r = rank_sh;
+    // T = D V_r Sigma_r^{-1/2}
+    for (int e = tid; e < p * r; e += blockDim.x) {
+      int i = e % p, t = e / p;
+      int kk = keep[t];
+      T[i + (size_t)t * p] = (dsc[i] / sqrt(sig[kk])) * V[i + kk * ld];
+    }
+    __syncthreads();
+    for (int e = tid; e < p * r; e += blockDim.x) {
+      int i = e % p, t = e / p;
+      cplx acc = mk(0, 0);
+      for (int j = 0; j < p; j++) acc = cfma(GA[i + (size_t)j * p], T[j + (size_t)t * p], acc);
+      U[i + (size_t)t * p] = acc;
+    }
+    __syncthreads();
+    rp = (r + 1) & ~1;
+    for (int e = tid; e < rp * rp; e += blockDim.x) {
+      int i = e % rp, j = e / rp;
+      cplx v = mk(0, 0);
+      if (i < r && j < r)
+        for (int k = 0; k < p; k++) v = v + cmulc(T[k + (size_t)i * p], U[k + (size_t)j * p]);
+      A[i + j * rp] = v;
+      V[i + j * rp] = mk(i == j ? 1.0 : 0.0, 0.0);
+    }
+    __syncthreads();
+    for (int e = tid; e < r * r; e += blockDim.x) {
+      int i = e % r, j = e / r;
+      if (i < j) {
+        cplx a = A[i + j * rp], b = A[j + i * rp];
+        cplx m = mk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
+        A[i + j * rp] = m;
+        A[j + i * rp] = conjg(m);
+      } else if (i == j) {
+        A[i + i * rp].y = 0.0;
+      }
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  // 4. eig of H
+  // 3. eig of H (r x r, ld rp)
   int sw = jacobi_smem(A, V, r, rp, rp, js, 40);
   for (int i = tid; i < r; i += blockDim.x) sig[i] = A[i + i * rp].x;
   __syncthreads();
   rank_sort(sig, r, order);
   __syncthreads();
-  // 5. C = T Q[:, order[:nb]]
   const int nout = min(nb, r);
-  for (int e = tid; e < p * nout; e += blockDim.x) {
-    int i = e % p, t = e / p;
-    int kk = order[t];
-    cplx acc = mk(0, 0);
-    for (int j = 0; j < r; j++) acc = cfma(T[i + (size_t)j * p], V[j + kk * rp], acc);
-    Cout[i + (size_t)t * p] = acc;
+  if (chol) {
+    // C = D L^{-H} Q_sel: L back into A (eigenvalues are in sig), then back substitution
+    // L^H Y = Q_sel row by row from the bottom (Y into U, global, ld p)
+    for (int e = tid; e < p * p; e += blockDim.x) {
+      int i = e % p, j = e / p;
+      A[i + j * ld] = Lg[e];
+    }
+    __syncthreads();
+    for (int i = p - 1; i >= 0; i--) {
+      const double inv = 1.0 / A[i + i * ld].x;
+      for (int t = tid; t < nout; t += blockDim.x) {
+        cplx acc = V[i + order[t] * rp];
+        for (int k = i + 1; k < p; k++) acc = acc - cmul(conjg(A[k + i * ld]), U[k + (size_t)t * p]);
+        U[i + (size_t)t * p] = inv * acc;
+      }
+      __syncthreads();
+    }
+    for (int e = tid; e < p * nout; e += blockDim.x) {
+      int i = e % p, t = e / p;
+      Cout[i + (size_t)t * p] = dsc[i] * U[i + (size_t)t * p];
+    }
+  } else {
+    for (int e = tid; e < p * nout; e += blockDim.x) {
+      int i = e % p, t = e / p;
+      int kk = order[t];
+      cplx acc = mk(0, 0);
+      for (int j = 0; j < r; j++) acc = cfma(T[i + (size_t)j * p], V[j + kk * rp], acc);
+      Cout[i + (size_t)t * p] = acc;
+    }
   }
   for (int t = tid; t < nout; t += blockDim.x) lam[t] = sig[order[t]];
   if (tid == 0) {
     info[0] = r;
     info[1] = sw;
+    info[2] = chol ? 1 : 0;
   }
 }
 

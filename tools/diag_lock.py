@@ -1,0 +1,20 @@
+import math, sys, time, numpy as np
+sys.path.insert(0, '.')
+import synth
+from paper_2511_17107_b200 import api
+PI = math.pi
+cases = [("vac8", np.eye(3), np.eye(3), np.zeros((4,8,8,8),np.uint8), 8, (PI,PI,PI), 6),
+         ("fcc8", synth.lattice("fcc"), synth.eps_pseudochiral(), synth.make_masks("random", synth.lattice("fcc"), 8, seed=3), 8, (0.7,-1.1,2.0), 10),
+         ("fcc16", synth.lattice("fcc"), synth.eps_pseudochiral(), synth.make_masks("fcc_diamond", synth.lattice("fcc"), 16), 16, (PI,PI,PI), 10),
+         ("sc32R", np.eye(3), synth.eps_pseudochiral(), synth.make_masks("sc_curv", np.eye(3), 32), 32, (PI,PI,PI), 10),
+         ("sc32G", np.eye(3), synth.eps_isotropic(13), synth.make_masks("sc_curv", np.eye(3), 32), 32, (0,0,0), 10)]
+for start in (0, 1):
+  for sticky in (1, 0):
+    for tol in (1e-5, 1e-7, 1e-9):
+        out = []
+        for name, A, e, m, n, k, nev in cases:
+            ctx = api.pc_create(A, n, e, m)
+            api.pc_set_option(ctx, "start", start); api.pc_set_option(ctx, "sticky_lock", sticky)
+            r = api.pc_bands(ctx, [k], nev=nev, tol=tol, maxit=300)
+            out.append(f"{name}:it{r['iters'][0]}{'' if r['status'][0]==0 else 'X'}")
+        print(f"start {start} sticky {sticky} tol {tol:.0e} ", " ".join(out), flush=True)
