@@ -14,14 +14,17 @@ static cudaError_t run_one(const ColPtrs& in, const MutColPtrs& out, const ColPt
   constexpr int N = PC_FFT_N;
   using Cfg = TileCfg<N, C>;
   auto kern = fft_pass_kernel<N, AXIS, DIR, OP, C>;
-  static bool attr_done = false;
-  if (!attr_done) {
+  static int occ = 0;
+  if (!occ) {
     cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     if (e != cudaSuccess) return e;
-    attr_done = true;
+    cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
+    if (occ < 1) occ = 1;
   }
-  dim3 grid((N / Cfg::TP) * N, C == 3 ? ncols : 3 * ncols);
-  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, xh, a);
+  const int ntiles = (N / Cfg::TP) * N * (C == 3 ? ncols : 3 * ncols);
+  const int grid = Cfg::STAGES > 1 ? std::min(ntiles, occ * 148) : ntiles;
+  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, xh, a, ntiles);
   return cudaGetLastError();
 }
 
@@ -37,4 +40,31 @@ cudaError_t PC_CAT(fft_launch_, PC_FFT_N)(int axis, int dir, int kind, const Col
   if (axis == 0) return run_one<0, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
   if (axis == 1) return run_one<1, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
   return run_one<2, +1, OP_NONE, 1>(in, out, xh, ncols, a, st);
+}
+
+#include "xex.cuh"
+
+template <int MODE>
+static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask, const EpsCoef& ec,
+                           const cplx* tw, double scale, cudaStream_t st) {
+  constexpr int N = PC_FFT_N;
+  using Cfg = XexCfg<N>;
+  auto kern = xex_kernel<N, MODE>;
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  dim3 grid((N / Cfg::TP) * N, ncols);
+  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale);
+  return cudaGetLastError();
+}
+
+cudaError_t PC_CAT(xex_launch_, PC_FFT_N)(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols,
+                                          const uint8_t* mask, const EpsCoef& ec, const cplx* tw, double scale,
+                                          cudaStream_t st) {
+  if (mode == 1) return run_xex<1>(in, out, ncols, mask, ec, tw, scale, st);
+  if (mode == 2) return run_xex<2>(in, out, ncols, mask, ec, tw, scale, st);
+  return run_xex<0>(in, out, ncols, mask, ec, tw, scale, st);
 }

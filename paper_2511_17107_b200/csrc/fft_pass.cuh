@@ -7,8 +7,8 @@
 // passes, TP whole rows for the x pass), transformed in shared memory by a two-step Stockham
 // split N = R1 * R2 (register codelets + one twiddle stage), and written back coalesced.
 //
-// Shared layout: s[(c*N + j)*TPP + p], TPP = TP + 1 (odd pitch: conflict-free 16-B accesses
-// both for p-fastest and j-fastest thread mappings).
+// Shared layout SI(c, j, p): y/z passes [c][j][p] (pitch TP+1), x pass [c][p][j] (pitch N+1) so that the
+// cp.async tile writes are contiguous like the HBM rows; odd pitches keep the FFT steps conflict-free.
 //
 // OP_KAH   (prologue): u = scale * (xhat x conj(kappa))   = K_A^H xhat
 // OP_KAG   (epilogue): y = kappa x s + gamma conj(kappa) (kappa . xhat)
@@ -61,7 +61,13 @@ struct TileCfg {
   static constexpr int TP = pow2_div(N, C == 3 ? 8 : 16);
   static constexpr int TPP = TP + 1;
   static constexpr int NT = TP * FftPlan<N>::R1;
-  static constexpr size_t SMEM = (size_t)C * N * TPP * sizeof(cplx) + (size_t)N * sizeof(cplx);
+  // x pass: [c][p][j] with pitch N+1 (tile rows contiguous as in HBM: conflict-free cp.async writes);
+  // y/z passes: [c][j][p] with pitch TP+1.  Both odd pitches: conflict-free 16-B fragment accesses.
+  static constexpr int SPAN = (TP * (N + 1) > N * TPP) ? TP * (N + 1) : N * TPP;
+  // C = 1: persistent CTAs with a 2-stage prefetch pipeline; C = 3 (fused symbol passes, 3x the tile):
+  // one tile per CTA and higher occupancy instead
+  static constexpr int STAGES = (C == 1) ? 2 : 1;
+  static constexpr size_t SMEM = (size_t)STAGES * C * SPAN * sizeof(cplx) + (size_t)N * sizeof(cplx);
 };
 
 // PassArgs: tw[j] = exp(-2 pi i j/N); ktab = [3 comps][3 axes][N] symbol pieces (OP_KAH/OP_KAG);
@@ -100,123 +106,143 @@ struct TileMap {
   }
 };
 
+// Persistent, double-buffered pass: CTA b processes tiles b, b + G, b + 2G, ...; the next tile streams
+// into the other shared-memory stage (cp.async) while the current one is transformed and written.
+// Tile index t -> (tile in volume t % TPV, column/component t / TPV).
 template <int N, int AXIS, int DIR, int OP, int C>
 __global__ void __launch_bounds__(TileCfg<N, C>::NT)
-fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a) {
+fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) {
   constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
   static_assert(R1 * R2 == N, "bad plan");
   constexpr int TP = TileCfg<N, C>::TP, TPP = TileCfg<N, C>::TPP, NT = TileCfg<N, C>::NT;
+  constexpr int SPAN = TileCfg<N, C>::SPAN;
   constexpr int N3 = N * N * N;
+  constexpr int TPV = (N / TP) * N;  // tiles per component volume
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* s = reinterpret_cast<cplx*>(smem_raw);
-  cplx* tw = s + C * N * TPP;
-
+  cplx* tw = reinterpret_cast<cplx*>(smem_raw);
+  cplx* stage_base = tw + N;  // [STAGES][C * SPAN]
+  constexpr int ST = TileCfg<N, C>::STAGES;
+  auto SI = [](int c, int j, int p) { return AXIS == 0 ? (c * TP + p) * (N + 1) + j : (c * N + j) * TPP + p; };
   const int tid = threadIdx.x;
-  const TileMap<N, AXIS, TP> tm(blockIdx.x);
-  int col, comp0;
-  if (C == 3) { col = blockIdx.y; comp0 = 0; }
-  else { col = blockIdx.y / 3; comp0 = blockIdx.y % 3; }
-  const cplx* gin = in.p[col] + (long long)comp0 * N3;
-  cplx* gout = out.p[col] + (long long)comp0 * N3;
 
-  // ---- stage tile into shared memory
-  for (int e = tid; e < C * N * TP; e += NT) {
-    int c, j, p;
-    if (AXIS == 0) { j = e % N; p = (e / N) % TP; c = e / (N * TP); }
-    else { p = e % TP; j = (e / TP) % N; c = e / (TP * N); }
-    cp_async16(&s[(c * N + j) * TPP + p], gin + (long long)c * N3 + tm.off(j, p));
-  }
-  cp_async_commit();
-  for (int j = tid; j < N; j += NT) tw[j] = ldg(a.tw + j);
-  cp_async_wait<0>();
-  __syncthreads();
-
-  // ---- prologue: u = scale * (xhat x conj(kappa))
-  if constexpr (OP == OP_KAH) {
-    for (int e = tid; e < N * TP; e += NT) {
-      int p = e % TP, j = e / TP;
-      int m1, m2, m3;
-      tm.modes(j, p, m1, m2, m3);
-      cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
-      cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
-      cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
-      cplx x1 = s[(0 * N + j) * TPP + p], x2 = s[(1 * N + j) * TPP + p], x3 = s[(2 * N + j) * TPP + p];
-      // (x x conj k)_1 = x2 ck3 - x3 ck2, _2 = x3 ck1 - x1 ck3, _3 = x1 ck2 - x2 ck1
-      cplx u1 = cmul(x2, conjg(k3)) - cmul(x3, conjg(k2));
-      cplx u2 = cmul(x3, conjg(k1)) - cmul(x1, conjg(k3));
-      cplx u3 = cmul(x1, conjg(k2)) - cmul(x2, conjg(k1));
-      s[(0 * N + j) * TPP + p] = a.scale * u1;
-      s[(1 * N + j) * TPP + p] = a.scale * u2;
-      s[(2 * N + j) * TPP + p] = a.scale * u3;
-    }
-    __syncthreads();
-  }
-
-  // ---- step A: R2 DFTs of size R1 (stride R2) + twiddle W_N^{j2 k1}; in place
-  for (int it = tid; it < C * TP * R2; it += NT) {
-    int p = it % TP, j2 = (it / TP) % R2, c = it / (TP * R2);
-    cplx v[R1];
-#pragma unroll
-    for (int j1 = 0; j1 < R1; j1++) v[j1] = s[(c * N + j2 + R2 * j1) * TPP + p];
-    Dft<R1, DIR>::run(v);
-#pragma unroll
-    for (int k1 = 0; k1 < R1; k1++) {
-      cplx w = tw[(j2 * k1) % N];
-      if (DIR > 0) w.y = -w.y;
-      s[(c * N + j2 + R2 * k1) * TPP + p] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
-    }
-  }
-  __syncthreads();
-
-  // ---- step B: R1 DFTs of size R2 (contiguous blocks) -> natural order k1 + R1 k2
-  {
-    const int p = tid % TP, k1 = tid / TP;  // NT = TP * R1: one item per thread per component
-#pragma unroll 1
-    for (int c = 0; c < C; c++) {
-      cplx v[R2];
-#pragma unroll
-      for (int j2 = 0; j2 < R2; j2++) v[j2] = s[(c * N + R2 * k1 + j2) * TPP + p];
-      Dft<R2, DIR>::run(v);
-      __syncthreads();
-#pragma unroll
-      for (int k2 = 0; k2 < R2; k2++) s[(c * N + k1 + R1 * k2) * TPP + p] = v[k2];
-    }
-  }
-  __syncthreads();
-
-  // ---- store (with fused epilogue)
-  if constexpr (OP == OP_KAG) {
-    const cplx* gx = xh.p[col];
-    for (int e = tid; e < N * TP; e += NT) {
-      int j, p;
-      if (AXIS == 0) { j = e % N; p = e / N; } else { p = e % TP; j = e / TP; }
-      int m1, m2, m3;
-      tm.modes(j, p, m1, m2, m3);
-      cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
-      cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
-      cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
-      int o = tm.off(j, p);
-      cplx x1 = ldg(gx + o), x2 = ldg(gx + N3 + o), x3 = ldg(gx + 2 * N3 + o);
-      cplx s1 = s[(0 * N + j) * TPP + p], s2 = s[(1 * N + j) * TPP + p], s3 = s[(2 * N + j) * TPP + p];
-      // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T)
-      cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
-      kx = a.gamma * kx;
-      cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), kx);
-      cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), kx);
-      cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), kx);
-      gout[o] = y1;
-      gout[N3 + o] = y2;
-      gout[2 * N3 + o] = y3;
-    }
-  } else {
-    const double sc = (OP == OP_NONE) ? a.scale : 1.0;  // OP_KAH applied it in the prologue
+  auto load_tile = [&](int t, cplx* s) {
+    const TileMap<N, AXIS, TP> tm(t % TPV);
+    const int cc = t / TPV;
+    const int col = (C == 3) ? cc : cc / 3, comp0 = (C == 3) ? 0 : cc % 3;
+    const cplx* gin = in.p[col] + (long long)comp0 * N3;
     for (int e = tid; e < C * N * TP; e += NT) {
       int c, j, p;
       if (AXIS == 0) { j = e % N; p = (e / N) % TP; c = e / (N * TP); }
       else { p = e % TP; j = (e / TP) % N; c = e / (TP * N); }
-      cplx v = s[(c * N + j) * TPP + p];
-      if (sc != 1.0) v = sc * v;
-      gout[(long long)c * N3 + tm.off(j, p)] = v;
+      cp_async16(&s[SI(c, j, p)], gin + (long long)c * N3 + tm.off(j, p));
     }
+  };
+
+  for (int j = tid; j < N; j += NT) tw[j] = ldg(a.tw + j);
+  int t = blockIdx.x;
+  if (t < ntiles) load_tile(t, stage_base);
+  cp_async_commit();
+  for (int it = 0; t < ntiles; t += gridDim.x, it++) {
+    cplx* s = stage_base + (it % ST) * C * SPAN;
+    if (ST > 1 && t + (int)gridDim.x < ntiles) load_tile(t + gridDim.x, stage_base + ((it + 1) % ST) * C * SPAN);
+    cp_async_commit();
+    cp_async_wait<1>();
+    __syncthreads();
+
+    const TileMap<N, AXIS, TP> tm(t % TPV);
+    const int cc = t / TPV;
+    const int col = (C == 3) ? cc : cc / 3, comp0 = (C == 3) ? 0 : cc % 3;
+    cplx* gout = out.p[col] + (long long)comp0 * N3;
+
+    // ---- prologue: u = scale * (xhat x conj(kappa))
+    if constexpr (OP == OP_KAH) {
+      for (int e = tid; e < N * TP; e += NT) {
+        int p = e % TP, j = e / TP;
+        int m1, m2, m3;
+        tm.modes(j, p, m1, m2, m3);
+        cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
+        cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
+        cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
+        cplx x1 = s[SI(0, j, p)], x2 = s[SI(1, j, p)], x3 = s[SI(2, j, p)];
+        // (x x conj k)_1 = x2 ck3 - x3 ck2, _2 = x3 ck1 - x1 ck3, _3 = x1 ck2 - x2 ck1
+        cplx u1 = cmul(x2, conjg(k3)) - cmul(x3, conjg(k2));
+        cplx u2 = cmul(x3, conjg(k1)) - cmul(x1, conjg(k3));
+        cplx u3 = cmul(x1, conjg(k2)) - cmul(x2, conjg(k1));
+        s[SI(0, j, p)] = a.scale * u1;
+        s[SI(1, j, p)] = a.scale * u2;
+        s[SI(2, j, p)] = a.scale * u3;
+      }
+      __syncthreads();
+    }
+
+    // ---- step A: R2 DFTs of size R1 (stride R2) + twiddle W_N^{j2 k1}; in place
+    for (int i = tid; i < C * TP * R2; i += NT) {
+      int p = i % TP, j2 = (i / TP) % R2, c = i / (TP * R2);
+      cplx v[R1];
+#pragma unroll
+      for (int j1 = 0; j1 < R1; j1++) v[j1] = s[SI(c, j2 + R2 * j1, p)];
+      Dft<R1, DIR>::run(v);
+#pragma unroll
+      for (int k1 = 0; k1 < R1; k1++) {
+        cplx w = tw[(j2 * k1) % N];
+        if (DIR > 0) w.y = -w.y;
+        s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+      }
+    }
+    __syncthreads();
+
+    // ---- step B: R1 DFTs of size R2 (contiguous blocks) -> natural order k1 + R1 k2
+    {
+      const int p = tid % TP, k1 = tid / TP;  // NT = TP * R1: one item per thread per component
+#pragma unroll 1
+      for (int c = 0; c < C; c++) {
+        cplx v[R2];
+#pragma unroll
+        for (int j2 = 0; j2 < R2; j2++) v[j2] = s[SI(c, R2 * k1 + j2, p)];
+        Dft<R2, DIR>::run(v);
+        __syncthreads();
+#pragma unroll
+        for (int k2 = 0; k2 < R2; k2++) s[SI(c, k1 + R1 * k2, p)] = v[k2];
+      }
+    }
+    __syncthreads();
+
+    // ---- store (with fused epilogue)
+    if constexpr (OP == OP_KAG) {
+      const cplx* gx = xh.p[col];
+      for (int e = tid; e < N * TP; e += NT) {
+        int j, p;
+        if (AXIS == 0) { j = e % N; p = e / N; } else { p = e % TP; j = e / TP; }
+        int m1, m2, m3;
+        tm.modes(j, p, m1, m2, m3);
+        cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
+        cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
+        cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
+        int o = tm.off(j, p);
+        cplx x1 = ldg(gx + o), x2 = ldg(gx + N3 + o), x3 = ldg(gx + 2 * N3 + o);
+        cplx s1 = s[SI(0, j, p)], s2 = s[SI(1, j, p)], s3 = s[SI(2, j, p)];
+        // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T)
+        cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
+        kx = a.gamma * kx;
+        cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), kx);
+        cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), kx);
+        cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), kx);
+        gout[o] = y1;
+        gout[N3 + o] = y2;
+        gout[2 * N3 + o] = y3;
+      }
+    } else {
+      const double sc = (OP == OP_NONE) ? a.scale : 1.0;  // OP_KAH applied it in the prologue
+      for (int e = tid; e < C * N * TP; e += NT) {
+        int c, j, p;
+        if (AXIS == 0) { j = e % N; p = (e / N) % TP; c = e / (N * TP); }
+        else { p = e % TP; j = (e / TP) % N; c = e / (TP * N); }
+        cplx v = s[SI(c, j, p)];
+        if (sc != 1.0) v = sc * v;
+        gout[(long long)c * N3 + tm.off(j, p)] = v;
+      }
+    }
+    __syncthreads();  // this stage is refilled by the prefetch issued in the next iteration
   }
+  cp_async_wait<0>();
 }

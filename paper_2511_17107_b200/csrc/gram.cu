@@ -1,0 +1,174 @@
+// Gram products G = S^H T of LOBPCG (the Rayleigh-Ritz projections) on the FP64
+// tensor pipe (DMMA mma.sync m8n8k4 f64).  Complex arithmetic on the real-interleaved view:
+//   Re G_mn = sum_k' a[m][k'] b[k'][n],  Im G_mn = sum_k' a[m][k'] b~[k'][n],
+//   a = S view, b = T view, b~[2k] = Im T_k, b~[2k+1] = -Re T_k  (4 real MACs per complex MAC).
+// CTA output block BM x BN = (WARPS_M*WM*8) x (WARPS_N*WN*8) complex; each warp owns WM x WN m8n8
+// tiles.  Rows stream through a STAGES-deep cp.async pipeline in chunks of KC complex rows.
+// Split-K over rows; partials reduced in a fixed order (deterministic).
+#include "kernels.h"
+#include "dmma.cuh"
+
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
+struct GramCfg {
+  static constexpr int BM = WARPS_M * WM * 8, BN = WARPS_N * WN * 8;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int PITCH = 2 * KC + 4;  // doubles per column: 8 mod 32 words -> conflict-free fragments
+  static constexpr size_t SMEM = (size_t)STAGES * (BM + BN) * PITCH * sizeof(double);
+};
+
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
+__global__ void __launch_bounds__(GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>::THREADS)
+gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_per_split, int nmb, cplx* partial) {
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
+  constexpr int BM = Cfg::BM, BN = Cfg::BN, NTH = Cfg::THREADS, PITCH = Cfg::PITCH;
+  extern __shared__ __align__(16) double gsm[];
+  double* As = gsm;                           // [STAGES][BM][PITCH]
+  double* Bs = gsm + STAGES * BM * PITCH;     // [STAGES][BN][PITCH]
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int mb = blockIdx.x % nmb, nb = blockIdx.x / nmb;
+  const int m0 = mb * BM, n0 = nb * BN;
+  const long long r0 = (long long)blockIdx.y * rows_per_split;
+  const long long r1 = min(len, r0 + rows_per_split);
+
+  double accR[WM][WN][2], accI[WM][WN][2];
+#pragma unroll
+  for (int i = 0; i < WM; i++)
+#pragma unroll
+    for (int j = 0; j < WN; j++) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
+
+  const cplx* dummy = S.p[0];
+  auto load_chunk = [&](int stage, long long rbase) {
+    for (int e = tid; e < (BM + BN) * KC; e += NTH) {
+      const int c = e / KC, r = e % KC;
+      const long long row = rbase + r;
+      const bool okr = row < r1;
+      double* dst;
+      const cplx* src = dummy;
+      bool ok;
+      if (c < BM) {
+        const int m = m0 + c;
+        ok = okr && m < p;
+        if (ok) src = S.p[m] + row;
+        dst = As + (stage * BM + c) * PITCH + 2 * r;
+      } else {
+        const int n = n0 + (c - BM);
+        ok = okr && n < q;
+        if (ok) src = T.p[n] + row;
+        dst = Bs + (stage * BN + (c - BM)) * PITCH + 2 * r;
+      }
+      cp_async16_zfill(dst, src, ok);
+    }
+  };
+
+  // warp tiles entirely outside [0, p) x [0, q) skip their MMAs (warp-uniform)
+  const bool live = (m0 + wm * WM * 8 < p) && (n0 + wn * WN * 8 < q);
+  const int nchunks = (r1 > r0) ? (int)((r1 - r0 + KC - 1) / KC) : 0;
+  // prologue: STAGES-1 chunks in flight (one commit group per chunk, empty groups allowed)
+#pragma unroll
+  for (int s = 0; s < STAGES - 1; s++) {
+    if (s < nchunks) load_chunk(s, r0 + (long long)s * KC);
+    cp_async_commit();
+  }
+  for (int ch = 0; ch < nchunks; ch++) {
+    const int nx = ch + STAGES - 1;
+    if (nx < nchunks) load_chunk(nx % STAGES, r0 + (long long)nx * KC);
+    cp_async_commit();
+    cp_async_wait<STAGES - 1>();
+    __syncthreads();
+    if (live) {
+      const int st = ch % STAGES;
+      const double* A = As + st * BM * PITCH;
+      const double* B = Bs + st * BN * PITCH;
+#pragma unroll 4
+      for (int s4 = 0; s4 < 2 * KC / 4; s4++) {
+        const int kk = 4 * s4 + (lane & 3);
+        double a[WM], b[WN], bi[WN];
+#pragma unroll
+        for (int mt = 0; mt < WM; mt++) a[mt] = A[(wm * WM * 8 + mt * 8 + (lane >> 2)) * PITCH + kk];
+#pragma unroll
+        for (int nt = 0; nt < WN; nt++) {
+          b[nt] = B[(wn * WN * 8 + nt * 8 + (lane >> 2)) * PITCH + kk];
+          const double bx = __shfl_xor_sync(0xffffffffu, b[nt], 1);
+          bi[nt] = (lane & 1) ? -bx : bx;
+        }
+#pragma unroll
+        for (int mt = 0; mt < WM; mt++)
+#pragma unroll
+          for (int nt = 0; nt < WN; nt++) {
+            dmma(accR[mt][nt][0], accR[mt][nt][1], a[mt], b[nt]);
+            dmma(accI[mt][nt][0], accI[mt][nt][1], a[mt], bi[nt]);
+          }
+      }
+    }
+    __syncthreads();  // the stage consumed here is refilled STAGES-1 iterations later
+  }
+  cp_async_wait<0>();
+
+  cplx* out = partial + (size_t)blockIdx.y * p * q;
+#pragma unroll
+  for (int mt = 0; mt < WM; mt++)
+#pragma unroll
+    for (int nt = 0; nt < WN; nt++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) {
+        const int m = m0 + wm * WM * 8 + mt * 8 + (lane >> 2);
+        const int n = n0 + wn * WN * 8 + nt * 8 + 2 * (lane & 3) + e;
+        if (m < p && n < q) out[(size_t)n * p + m] = mk(accR[mt][nt][e], accI[mt][nt][e]);
+      }
+}
+
+__global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx* G) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= pq) return;
+  cplx acc = mk(0, 0);
+  for (int s = 0; s < nsplit; s++) acc = acc + partial[(size_t)s * pq + idx];
+  G[idx] = acc;
+}
+
+size_t gram_partial_bytes(int p, int q) { return (size_t)4 * 148 * p * q * sizeof(cplx) + 4096; }
+
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
+static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
+                     cudaStream_t st) {
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
+  auto kern = gram_kernel<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
+  static int ctas_per_sm = 0;
+  if (!ctas_per_sm) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, Cfg::THREADS, Cfg::SMEM);
+    ctas_per_sm = std::max(1, ctas_per_sm);
+  }
+  const int nmb = (p + Cfg::BM - 1) / Cfg::BM, nnb = (q + Cfg::BN - 1) / Cfg::BN;
+  const int nblk = nmb * nnb;
+  int ns = std::max(1, (ctas_per_sm * 148 + nblk - 1) / nblk);
+  ns = std::min(ns, 4 * 148);
+  ns = (int)std::max(1LL, std::min<long long>(ns, (len + 4 * KC - 1) / (4 * KC)));
+  long long rps = (len + ns - 1) / ns;
+  rps = (rps + KC - 1) / KC * KC;
+  ns = (int)((len + rps - 1) / rps);
+  kern<<<dim3(nblk, ns), Cfg::THREADS, Cfg::SMEM, st>>>(S, p, T, q, len, rps, nmb, partial);
+  const int pq = p * q;
+  gram_reduce_kernel<<<(pq + 255) / 256, 256, 0, st>>>(partial, ns, pq, G);
+}
+
+// Block shape: least padded output area, then most warps per CTA.
+void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
+                 cudaStream_t st) {
+  struct Opt { int bm, bn; };
+  const Opt opts[4] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}};
+  int best = 0;
+  double best_cost = 1e300;
+  for (int i = 0; i < 4; i++) {
+    const double area = (double)((p + opts[i].bm - 1) / opts[i].bm * opts[i].bm) *
+                        ((q + opts[i].bn - 1) / opts[i].bn * opts[i].bn);
+    const double cost = area * (1.0 + 0.03 * i);
+    if (cost < best_cost) { best_cost = cost; best = i; }
+  }
+  switch (best) {
+    case 0: run_gram<3, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 256 thr, 97 KB
+    case 1: run_gram<3, 2, 2, 3, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 192 thr, 83 KB
+    case 2: run_gram<2, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 256 thr, 83 KB
+    default: run_gram<2, 2, 2, 2, 16, 3>(S, p, T, q, len, G, partial, st); break;  // 128 thr, 55 KB
+  }
+}

@@ -38,6 +38,11 @@ int fft_supported_list(int* sizes, int cap);
 cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
                             const ColPtrs& xh, int ncols, const PassArgsH& a, cudaStream_t st);
 
+// fused x-inverse DFT + M_eps + x-forward DFT (media with eps_13 = eps_23 = 0 in CrossDoF mode; any
+// Diagonal/Trivial medium): in -> out (must differ), output scaled by `scale`.
+cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
+                       const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st);
+
 // pointwise ---------------------------------------------------------------------------------
 void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t st);
 void launch_precond(const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const cplx* kt, double gamma,

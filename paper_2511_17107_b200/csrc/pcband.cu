@@ -90,6 +90,7 @@ struct pc_ctx {
   int p_restart = 1;  // drop the P block when the Rayleigh-Ritz basis is rank deficient
   int sticky_lock = 0;         // 1: locked columns stay locked (SciPy's activeMask &=); 0: may re-activate
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
+  int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
   DevBuf pwbuf;
@@ -369,6 +370,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "start") c->start_mode = (int)v;
   else if (k == "sticky_lock") c->sticky_lock = (int)v;
   else if (k == "gram_refresh") c->gram_refresh = (int)v;
+  else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
@@ -452,6 +454,29 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   {
     Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 30.0 * pts, 96.0 * pts);
     CHK(fft_pass(c, 2, +1, 1, X, Y, none, nc, inv_n3, st));
+  }
+  // z-plane-local media (eps_13 = eps_23 = 0 in CrossDoF; any Diagonal/Trivial medium): the x-passes
+  // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
+  const bool plane_local = c->fuse_xex && (c->eps_mode != PC_EPS_CROSSDOF || (!c->ec.has[1] && !c->ec.has[2]));
+  if (plane_local) {
+    {
+      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+      CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
+    }
+    {
+      Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 100.0 * pts, 96.0 * pts);
+      cudaError_t e = launch_xex(n, c->eps_mode, Yc, WS, nc, c->d_mask, c->ec, c->d_tw, 1.0, st);
+      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
+    }
+    {
+      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+      CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
+    }
+    {
+      Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 40.0 * pts, 144.0 * pts);
+      CHK(fft_pass(c, 2, -1, 2, Wc, Y, X, nc, 1.0, st));
+    }
+    return PC_OK;
   }
   {
     Prof p(c, PC_STAT_FFT_MID, st, 2, 2 * fl, 2 * 96.0 * pts);

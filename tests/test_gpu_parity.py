@@ -208,3 +208,25 @@ def test_device_jacobi_eigh(api, n):
     assert np.allclose(w, wr, rtol=1e-12, atol=1e-12 * np.abs(wr).max())
     assert np.allclose(V.conj().T @ V, np.eye(n), atol=1e-12)
     assert np.linalg.norm(M @ V - V * w[None, :]) <= 1e-12 * np.linalg.norm(M)
+
+
+@pytest.mark.parametrize("eps,mode,n", [("pc", "crossdof", 16), ("iso", "crossdof", 12), ("sdd", "trivial", 8),
+                                        ("pc", "crossdof", 128)])
+def test_fused_xex_pipeline_matches_unfused(api, eps, mode, n):
+    """The fused x-DFT + M_eps + x-DFT pass (z-plane-local media) against the 7-pass pipeline and the oracle."""
+    A = synth.lattice("fcc")
+    e = _eps(eps)
+    masks = synth.make_masks("fcc_diamond" if n > 16 else "random", A, n, seed=13)
+    ctx = api.pc_create(A, n, e, masks, eps_mode=mode)
+    k = (PI, 0.4, -1.3)
+    X = torch.randn(3, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    Y1 = torch.empty_like(X)
+    Y0 = torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y1)
+    api.pc_set_option(ctx, "fuse_xex", 0)
+    api.pc_apply(ctx, k, X, Y0)
+    err = (torch.linalg.vector_norm(Y1 - Y0, dim=1) / torch.linalg.vector_norm(Y0, dim=1)).max().item()
+    assert err <= 1e-13
+    if n <= 16:
+        op = O.PenalizedOperator(n, np.array(k), A, e, masks, mode)
+        assert relerr_cols(Y1.cpu().numpy(), op.apply_fourier(X.cpu().numpy())) <= 1e-12
