@@ -204,6 +204,7 @@ def main():
     ap.add_argument("--apply-cols", type=int, default=15)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
+    ap.add_argument("--guard", type=int, default=None, help="LOBPCG guard columns (block = nev + guard)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -233,6 +234,8 @@ def main():
     kp = W.kpoints()
     nk = len(kp)
     ctx = api.pc_create(A, W.n, eps1, masks, device=local)
+    if args.guard is not None:
+        api.pc_set_option(ctx, "guard", args.guard)
 
     def kidx(s):
         return (rank + world * s) % nk
@@ -358,12 +361,13 @@ def main():
         try:
             cores = len(os.sched_getaffinity(0))
             _, tcomp = oracle_sample(W, kk, 1, masks=masks)
-            v, per_it = oracle_kpts_per_s(tcomp, float(np.mean(iters)))
+            v, per_it = oracle_kpts_per_s(tcomp, PAPER_ITERS_FCC_PC)
             cpu = {"value": v, "unit": "k-points/s", "cores": cores, "kind": "oracle",
                    "sample": f"oracle sparse assembly at n={W.n} + 1 apply + 1 K_P^-1 column + one 3b-column Gram "
-                             f"timed; k-point modelled as assembly + {np.mean(iters):.1f} iterations (this run's "
-                             f"GPU mean) x (b={W.nev + 5} applies+precond + 2 Grams) = "
-                             f"{tcomp['assembly_s']:.1f} s + {np.mean(iters):.1f} x {per_it:.1f} s",
+                             f"timed; k-point modelled as assembly + {PAPER_ITERS_FCC_PC} iterations (PAPER.md:1199; "
+                             f"same model as --impl reference; this GPU run needed {np.mean(iters):.1f}) x "
+                             f"(b={W.nev + 5} applies+precond + 2 Grams) = "
+                             f"{tcomp['assembly_s']:.1f} s + {PAPER_ITERS_FCC_PC} x {per_it:.1f} s",
                    "components": tcomp}
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "error": str(ex)}

@@ -60,7 +60,7 @@ struct XexCfg {
 
 // MODE: 0 diagonal, 1 crossdof with only eps_12, 2 trivial
 template <int N, int MODE>
-__global__ void __launch_bounds__(XexCfg<N>::NT)
+__global__ void __launch_bounds__(XexCfg<N>::NT, 3)
 xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
            double scale) {
   using Cfg = XexCfg<N>;
@@ -76,9 +76,21 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   const cplx* gin = in.p[col];
   cplx* gout = out.p[col];
 
-  // stage rows y0-1 .. y0+TP of the three components (and their mask bytes)
-  for (int e = tid; e < 3 * RP * N; e += NT) {
-    const int j = e % N, r = (e / N) % RP, c = e / (N * RP);
+  // Rows held per component (smem row r <-> y = y0 - 1 + r): S_12^T v1 needs E^1 at y0-1 (r = 0),
+  // S_12 v2 needs E^2 at y0+TP (r = TP+1); E^3 and the pointwise modes need only r = 1..TP.
+  // pencil list: component 0 rows [lo0, lo0+n0), component 1 rows [1, 1+n1), component 2 rows [1, 1+TP)
+  constexpr int n0 = (MODE == 1) ? TP + 1 : TP, lo0 = (MODE == 1) ? 0 : 1;
+  constexpr int n1 = (MODE == 1) ? TP + 1 : TP;
+  constexpr int NPEN = n0 + n1 + TP;
+  auto pen_row = [&](int pen, int& c, int& r) {
+    if (pen < n0) { c = 0; r = lo0 + pen; }
+    else if (pen < n0 + n1) { c = 1; r = 1 + pen - n0; }
+    else { c = 2; r = 1 + pen - n0 - n1; }
+  };
+  for (int e = tid; e < NPEN * N; e += NT) {
+    const int j = e % N;
+    int c, r;
+    pen_row(e / N, c, r);
     const int y = (y0 - 1 + r + N) % N;
     cp_async16(&s[(c * RP + r) * NP1 + j], gin + (long long)c * N3 + ((long long)z * N + y) * N + j);
   }
@@ -100,8 +112,12 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   cp_async_wait<0>();
   __syncthreads();
 
-  // inverse x-DFT of all 3*RP rows
-  smem_fft<N, +1>(s, tw, 3 * RP, [&](int pen, int j) { return pen * NP1 + j; });
+  // inverse x-DFT of the held rows
+  smem_fft<N, +1>(s, tw, NPEN, [&](int pen, int j) {
+    int c, r;
+    pen_row(pen, c, r);
+    return (c * RP + r) * NP1 + j;
+  });
 
   // M_eps on the TP output rows (registers first: the stencil reads neighbours)
   cplx w[PPT][3];
