@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--guard", type=int, default=None, help="LOBPCG guard columns (block = nev + guard)")
+    ap.add_argument("--w-guard", type=int, default=None, help="guard columns that get search directions")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -236,6 +237,8 @@ def main():
     ctx = api.pc_create(A, W.n, eps1, masks, device=local)
     if args.guard is not None:
         api.pc_set_option(ctx, "guard", args.guard)
+    if args.w_guard is not None:
+        api.pc_set_option(ctx, "w_guard", args.w_guard)
 
     def kidx(s):
         return (rank + world * s) % nk

@@ -152,23 +152,33 @@ static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long
   gram_reduce_kernel<<<(pq + 255) / 256, 256, 0, st>>>(partial, ns, pq, G);
 }
 
-// Block shape: least padded output area, then most warps per CTA.
+// Block shape: least padded output area (the DMMA pipe is the bound, padding is wasted MMAs), ties
+// broken towards fewer CTA blocks per output.
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                  cudaStream_t st) {
   struct Opt { int bm, bn; };
-  const Opt opts[4] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}};
+  const Opt opts[] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}, {40, 40}, {40, 64}, {64, 64}, {80, 64},
+                      {80, 96}, {24, 32}, {48, 96}};
+  const int nopt = sizeof(opts) / sizeof(opts[0]);
   int best = 0;
   double best_cost = 1e300;
-  for (int i = 0; i < 4; i++) {
-    const double area = (double)((p + opts[i].bm - 1) / opts[i].bm * opts[i].bm) *
-                        ((q + opts[i].bn - 1) / opts[i].bn * opts[i].bn);
-    const double cost = area * (1.0 + 0.03 * i);
-    if (cost < best_cost) { best_cost = cost; best = i; }
+  for (int i = 0; i < nopt; i++) {
+    const int nbm = (p + opts[i].bm - 1) / opts[i].bm, nbn = (q + opts[i].bn - 1) / opts[i].bn;
+    const double area = (double)nbm * opts[i].bm * nbn * opts[i].bn;
+    const double cost = area * (1.0 + 0.04 * (nbm * nbn - 1));
+    if (cost < best_cost - 1e-9) { best_cost = cost; best = i; }
   }
   switch (best) {
-    case 0: run_gram<3, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 256 thr, 97 KB
-    case 1: run_gram<3, 2, 2, 3, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 192 thr, 83 KB
-    case 2: run_gram<2, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;   // 256 thr, 83 KB
-    default: run_gram<2, 2, 2, 2, 16, 3>(S, p, T, q, len, G, partial, st); break;  // 128 thr, 55 KB
+    case 0: run_gram<3, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 1: run_gram<3, 2, 2, 3, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 2: run_gram<2, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 3: run_gram<2, 2, 2, 2, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 4: run_gram<5, 1, 1, 5, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 5: run_gram<5, 1, 1, 8, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 6: run_gram<4, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 7: run_gram<5, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 8: run_gram<5, 3, 2, 4, 16, 2>(S, p, T, q, len, G, partial, st); break;
+    case 9: run_gram<3, 1, 1, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    default: run_gram<3, 3, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
   }
 }

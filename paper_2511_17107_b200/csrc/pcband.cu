@@ -91,6 +91,7 @@ struct pc_ctx {
   int sticky_lock = 0;         // 1: locked columns stay locked (SciPy's activeMask &=); 0: may re-activate
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
+  int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
   DevBuf pwbuf;
@@ -371,6 +372,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "sticky_lock") c->sticky_lock = (int)v;
   else if (k == "gram_refresh") c->gram_refresh = (int)v;
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
+  else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
@@ -871,14 +873,16 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   bool haveP = false;
   int it = 0, conv = 0;
   for (;; it++) {
-    // residuals, K_P^{-1} R for every column
+    // residuals of every column; W = K_P^{-1} R only for the columns that can receive a search direction
     {
-      Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 3.0 * 16.0 * len * b);
+      const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
+      Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + nw));
       ColPtrs X, AX;
       MutColPtrs W;
       ccols(sX, all, X, 0);
       ccols(sAX, all, AX, 0);
       mcols(WW, all, W, 0);
+      for (int j = nw; j < b; j++) W.p[j] = nullptr;
       launch_resid(X, AX, W, dLam, b, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dNorm, st);
     }
     cudaMemcpyAsync(hN, dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
@@ -894,6 +898,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       // re-enters if its residual rises above tol again
       if (!(res[j] > tol)) active[j] = 0;
       else if (!c->sticky_lock) active[j] = 1;
+      // guard columns beyond nev + w_guard never get a search direction (they ride along in X and P)
+      if (c->w_guard >= 0 && j >= nev + c->w_guard) active[j] = 0;
       if (j < nev && res[j] > tol) conv = 0;
     }
     if (c->verbose) {
