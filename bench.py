@@ -205,6 +205,7 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--guard", type=int, default=None, help="LOBPCG guard columns (block = nev + guard)")
+    ap.add_argument("--streams", type=int, default=2, help="concurrent k-point solves per GPU (contexts)")
     ap.add_argument("--w-guard", type=int, default=None, help="guard columns that get search directions")
     args = ap.parse_args()
     if args.impl == "reference":
@@ -234,48 +235,62 @@ def main():
     masks = W.masks()
     kp = W.kpoints()
     nk = len(kp)
-    ctx = api.pc_create(A, W.n, eps1, masks, device=local)
-    if args.guard is not None:
-        api.pc_set_option(ctx, "guard", args.guard)
-    if args.w_guard is not None:
-        api.pc_set_option(ctx, "w_guard", args.w_guard)
+    ctxs = [api.pc_create(A, W.n, eps1, masks, device=local) for _ in range(max(1, args.streams))]
+    for c_ in ctxs:
+        if args.guard is not None:
+            api.pc_set_option(c_, "guard", args.guard)
+        if args.w_guard is not None:
+            api.pc_set_option(c_, "w_guard", args.w_guard)
+    ctx = ctxs[0]
 
     def kidx(s):
         return (rank + world * s) % nk
 
-    # warm-up: W solves (allocations, first-touch, kernel attribute setup)
-    wit = []
-    for s in range(args.warmup):
-        om, rs, it, st = bands.solve_local(ctx, kp, [kidx(s)], W.nev, args.tol, args.maxit, 0)
-        wit.append(int(it[0]))
-    api.pc_stats(ctx, reset=True)
-    api.pc_set_option(ctx, "profile", 1)
+    def run(idx_list):
+        if len(ctxs) == 1:
+            return bands.solve_local(ctx, kp, idx_list, W.nev, args.tol, args.maxit, 0)
+        return bands.solve_concurrent(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
+
+    # warm-up: W solves (at least one per context: allocations, first touch, kernel attributes)
+    nwarm = max(args.warmup, len(ctxs))
+    wit = [int(v) for v in run([kidx(s) for s in range(nwarm)])[2]]
+    for c_ in ctxs:
+        api.pc_stats(c_, reset=True)
+        api.pc_set_option(c_, "profile", 1)
     clk = Clocks(local)
     barrier()
     clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    idx = [kidx(s) for s in range(nwarm, nwarm + args.steps)]
     e0.record()
-    res = []
-    for s in range(args.warmup, args.warmup + args.steps):
-        res.append(bands.solve_local(ctx, kp, [kidx(s)], W.nev, args.tol, args.maxit, 0))
+    om, rs, it_, st_ = run(idx)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
     clocks = clk.stop()
     barrier()
-    stats = api.pc_stats(ctx)
-    api.pc_set_option(ctx, "profile", 0)
+    stats = None
+    for c_ in ctxs:
+        s_ = api.pc_stats(c_)
+        api.pc_set_option(c_, "profile", 0)
+        if stats is None:
+            stats = s_
+        else:
+            for k_, v_ in s_.items():
+                if isinstance(v_, dict):
+                    for f_ in v_:
+                        stats[k_][f_] += v_[f_]
+                else:
+                    stats[k_] += v_
     t = torch.tensor([ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
     value = world * args.steps / (ms_max / 1000.0)
+    res = [(om[i:i + 1], rs[i:i + 1], it_[i:i + 1], st_[i:i + 1]) for i in range(len(idx))]
     iters = [int(r[2][0]) for r in res]
     status = [int(r[3][0]) for r in res]
     # the one collective of the method: all-gather of eigenvalues
-    idx = [kidx(s) for s in range(args.warmup, args.warmup + args.steps)]
-    om = np.concatenate([r[0] for r in res])
-    rs = np.concatenate([r[1] for r in res])
     gathered = None
     if world > 1:
         loc = torch.from_numpy(np.concatenate([np.array(idx)[:, None], om], axis=1)).to(dev)
@@ -380,7 +395,8 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": workload_config(W, args) | {"kpoints_per_rank": args.steps,
-                                                      "parallelism": f"k-path sharded over {world} GPU(s)"},
+                                                      "parallelism": f"k-path sharded over {world} GPU(s), "
+                                                                     f"{len(ctxs)} concurrent k-point solve(s) per GPU"},
                 "iters": iters, "status": status, "warmup_iters": wit,
                 "omega2_first_k": om[0].tolist(), "resid_max": float(rs.max()),
                 "apply": apply, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
@@ -391,7 +407,8 @@ def main():
                                    for k, v in cls.items()},
                 "gathered_rows": gathered}
         print(json.dumps(line), flush=True)
-    ctx.close()
+    for c_ in ctxs:
+        c_.close()
     if world > 1:
         dist.destroy_process_group()
 

@@ -38,6 +38,47 @@ def solve_local(ctx, kpts: np.ndarray, idx: list, nev: int, tol: float, maxit: i
     return om, rs, it, stt
 
 
+def solve_concurrent(ctxs, kpts: np.ndarray, idx: list, nev: int, tol: float, maxit: int, seed: int):
+    """Solve the k-points idx with len(ctxs) independent contexts on one GPU, one host thread each
+    (each context owns its CUDA stream and workspace; ctypes releases the GIL during pc_bands), so
+    the single-CTA Rayleigh-Ritz steps and host round trips of one k-point overlap the bulk kernels
+    of another.  Work is handed out from a shared queue in index order; results are independent of
+    the number of contexts (start blocks are keyed by the global k index)."""
+    import threading
+    from . import api
+    om = np.zeros((len(idx), nev))
+    rs = np.zeros((len(idx), nev))
+    it = np.zeros(len(idx), dtype=np.int64)
+    stt = np.zeros(len(idx), dtype=np.int64)
+    lock = threading.Lock()
+    nxt = [0]
+    errors = []
+
+    def worker(ctx):
+        try:
+            while True:
+                with lock:
+                    t = nxt[0]
+                    nxt[0] += 1
+                if t >= len(idx):
+                    return
+                g = idx[t]
+                api.pc_set_option(ctx, "kindex_offset", g)
+                r = api.pc_bands(ctx, kpts[g:g + 1], nev=nev, tol=tol, maxit=maxit, seed=seed)
+                om[t], rs[t], it[t], stt[t] = r["omega2"][0], r["resid"][0], r["iters"][0], r["status"][0]
+        except Exception as ex:  # pragma: no cover - surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(c,)) for c in ctxs]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    return om, rs, it, stt
+
+
 def gather(om, rs, it, stt, idx, nk, group=None, device=None):
     """All-gather the per-rank results (one collective) and scatter them into k order."""
     import torch
