@@ -214,6 +214,14 @@ int pc_debug_heevj(const double *A_host, int n, double *w_host, double *V_host, 
 int pc_debug_pass(pc_ctx *ctx, const double k[3], int kind, int axis, int dir, const void *X, void *Y,
                   const void *XH, int ncols, long long ld, double scale);
 
+/*
+ * pc_history — residual history of the last k-point solved by pc_bands on this context: returns the
+ * number of iterations R recorded; *block = b (columns); out (host, may be NULL) receives
+ * min(R, cap) rows of b doubles Res_j, one row per LOBPCG iteration (row 0 = start
+ * block after the first Rayleigh-Ritz step).  Used for the asymptotic damping factor theta.
+ */
+int pc_history(const pc_ctx *ctx, double *out, int cap, int *block);
+
 /* Supported grid sizes: writes up to cap values into sizes, returns how many exist. */
 int pc_supported_n(int *sizes, int cap);
 

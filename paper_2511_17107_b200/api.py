@@ -58,6 +58,7 @@ def lib():
         "pc_stats": (i, [vp, dp, i]),
         "pc_supported_n": (i, [ip, i]),
         "pc_debug_heevj": (i, [dp, i, dp, dp, ip]),
+        "pc_history": (i, [vp, dp, i, ip]),
         "pc_destroy": (None, [vp]),
         "pc_last_error": (ctypes.c_char_p, []),
     }
@@ -214,6 +215,15 @@ def pc_stats(ctx: Ctx, reset=False):
                "bytes": float(out[4 * i + 3])} for i, nm in enumerate(STAT_NAMES)}
     st["launches"] = int(out[-1])
     return st
+
+
+def pc_history(ctx: Ctx):
+    """(iterations, b) array of Res_j for the last solved k-point."""
+    b = ctypes.c_int()
+    rows = lib().pc_history(ctx.h, None, 0, ctypes.byref(b))
+    out = np.zeros(max(1, rows * b.value))
+    lib().pc_history(ctx.h, _dptr(out), rows, ctypes.byref(b))
+    return out[: rows * b.value].reshape(rows, b.value)
 
 
 def pc_debug_heevj(A):

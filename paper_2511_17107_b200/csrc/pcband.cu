@@ -95,6 +95,8 @@ struct pc_ctx {
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
   DevBuf pwbuf;
+  std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
+  int hist_b = 0;
   // LOBPCG storage
   DevBuf lob, small, gpart;
   double* h_pinned = nullptr;
@@ -376,6 +378,16 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
+}
+
+extern "C" int pc_history(const pc_ctx* c, double* out, int cap, int* block) {
+  if (!c) return set_err(PC_EINVAL, "pc_history: null ctx");
+  const int b = c->hist_b;
+  const int rows = b ? (int)(c->hist.size() / b) : 0;
+  if (block) *block = b;
+  if (out)
+    for (int i = 0; i < std::min(rows, cap) * b; i++) out[i] = c->hist[i];
+  return rows;
 }
 
 extern "C" int pc_stats(pc_ctx* c, double* out, int reset) {
@@ -870,6 +882,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
 
   std::vector<char> active(b, 1);
   std::vector<double> res(b, 0.0);
+  c->hist.clear();
+  c->hist_b = b;
   bool haveP = false;
   int it = 0, conv = 0;
   for (;; it++) {
@@ -894,6 +908,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     conv = 1;
     for (int j = 0; j < b; j++) {
       res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
+      c->hist.push_back(res[j]);
       // soft locking: a converged column leaves the search block (no W, P); with sticky_lock = 0 it
       // re-enters if its residual rises above tol again
       if (!(res[j] > tol)) active[j] = 0;
