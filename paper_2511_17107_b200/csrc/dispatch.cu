@@ -9,7 +9,7 @@ PC_FFT_SIZES(PC_DECL)
 #undef PC_DECL
 #define PC_DECL2(N)                                                                                       \
   cudaError_t xex_launch_##N(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask, \
-                             const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st);
+                             const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st);
 PC_FFT_SIZES(PC_DECL2)
 #undef PC_DECL2
 
@@ -39,9 +39,9 @@ cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& i
 }
 
 cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
-                       const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st) {
+                       const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st) {
   switch (n) {
-#define PC_SW2(N) case N: return xex_launch_##N(mode, in, out, ncols, mask, ec, tw, scale, st);
+#define PC_SW2(N) case N: return xex_launch_##N(mode, in, out, ncols, mask, ec, tw, scale, z0, nz, st);
     PC_FFT_SIZES(PC_SW2)
 #undef PC_SW2
     default: return cudaErrorInvalidValue;

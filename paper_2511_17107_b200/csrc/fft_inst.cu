@@ -22,7 +22,8 @@ static cudaError_t run_one(const ColPtrs& in, const MutColPtrs& out, const ColPt
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
     if (occ < 1) occ = 1;
   }
-  const int ntiles = (N / Cfg::TP) * N * (C == 3 ? ncols : 3 * ncols);
+  const int nzp = (AXIS != 2 && a.nz > 0) ? a.nz : N;
+  const int ntiles = (N / Cfg::TP) * nzp * (C == 3 ? ncols : 3 * ncols);
   const int grid = Cfg::STAGES > 1 ? std::min(ntiles, occ * 148) : ntiles;
   kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, xh, a, ntiles);
   return cudaGetLastError();
@@ -46,7 +47,7 @@ cudaError_t PC_CAT(fft_launch_, PC_FFT_N)(int axis, int dir, int kind, const Col
 
 template <int MODE>
 static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask, const EpsCoef& ec,
-                           const cplx* tw, double scale, cudaStream_t st) {
+                           const cplx* tw, double scale, int z0, int nz, cudaStream_t st) {
   constexpr int N = PC_FFT_N;
   using Cfg = XexCfg<N>;
   auto kern = xex_kernel<N, MODE>;
@@ -56,15 +57,15 @@ static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  dim3 grid((N / Cfg::TP) * N, ncols);
-  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale);
+  dim3 grid((N / Cfg::TP) * (nz > 0 ? nz : N), ncols);
+  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale, nz > 0 ? z0 : 0);
   return cudaGetLastError();
 }
 
 cudaError_t PC_CAT(xex_launch_, PC_FFT_N)(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols,
                                           const uint8_t* mask, const EpsCoef& ec, const cplx* tw, double scale,
-                                          cudaStream_t st) {
-  if (mode == 1) return run_xex<1>(in, out, ncols, mask, ec, tw, scale, st);
-  if (mode == 2) return run_xex<2>(in, out, ncols, mask, ec, tw, scale, st);
-  return run_xex<0>(in, out, ncols, mask, ec, tw, scale, st);
+                                          int z0, int nz, cudaStream_t st) {
+  if (mode == 1) return run_xex<1>(in, out, ncols, mask, ec, tw, scale, z0, nz, st);
+  if (mode == 2) return run_xex<2>(in, out, ncols, mask, ec, tw, scale, z0, nz, st);
+  return run_xex<0>(in, out, ncols, mask, ec, tw, scale, z0, nz, st);
 }

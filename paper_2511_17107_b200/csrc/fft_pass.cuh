@@ -86,9 +86,9 @@ struct TileMap {
   int base;   // offset of (j=0, p=0)
   int sj, sp; // strides of j and p
   int fixed_a, fixed_b;
-  DEV TileMap(int t) {
+  DEV TileMap(int t, int qoff = 0) {
     constexpr int NT_ = N / TP;
-    int q = t / NT_, r = (t % NT_) * TP;
+    int q = t / NT_ + (AXIS == 2 ? 0 : qoff), r = (t % NT_) * TP;
     if (AXIS == 2) {        // pencils along z, tile = TP consecutive x at fixed y = q
       base = q * N + r; sj = N * N; sp = 1; fixed_a = q; fixed_b = r;
     } else if (AXIS == 1) { // pencils along y, tile = TP consecutive x at fixed z = q
@@ -117,7 +117,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
   constexpr int TP = TileCfg<N, C>::TP, TPP = TileCfg<N, C>::TPP, NT = TileCfg<N, C>::NT;
   constexpr int SPAN = TileCfg<N, C>::SPAN;
   constexpr int N3 = N * N * N;
-  constexpr int TPV = (N / TP) * N;  // tiles per component volume
+  const int TPV = (N / TP) * ((AXIS != 2 && a.nz > 0) ? a.nz : N);  // tiles per component volume (z-range)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* tw = reinterpret_cast<cplx*>(smem_raw);
   cplx* stage_base = tw + N;  // [STAGES][C * SPAN]
@@ -126,7 +126,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
   const int tid = threadIdx.x;
 
   auto load_tile = [&](int t, cplx* s) {
-    const TileMap<N, AXIS, TP> tm(t % TPV);
+    const TileMap<N, AXIS, TP> tm(t % TPV, a.z0);
     const int cc = t / TPV;
     const int col = (C == 3) ? cc : cc / 3, comp0 = (C == 3) ? 0 : cc % 3;
     const cplx* gin = in.p[col] + (long long)comp0 * N3;
@@ -149,7 +149,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
     cp_async_wait<1>();
     __syncthreads();
 
-    const TileMap<N, AXIS, TP> tm(t % TPV);
+    const TileMap<N, AXIS, TP> tm(t % TPV, a.z0);
     const int cc = t / TPV;
     const int col = (C == 3) ? cc : cc / 3, comp0 = (C == 3) ? 0 : cc % 3;
     cplx* gout = out.p[col] + (long long)comp0 * N3;

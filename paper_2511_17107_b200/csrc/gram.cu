@@ -1,7 +1,8 @@
 // Gram products G = S^H T of LOBPCG (the Rayleigh-Ritz projections) on the FP64
-// tensor pipe (DMMA mma.sync m8n8k4 f64).  Complex arithmetic on the real-interleaved view:
-//   Re G_mn = sum_k' a[m][k'] b[k'][n],  Im G_mn = sum_k' a[m][k'] b~[k'][n],
-//   a = S view, b = T view, b~[2k] = Im T_k, b~[2k+1] = -Re T_k  (4 real MACs per complex MAC).
+// tensor pipe (DMMA mma.sync m8n8k4 f64).  Complex arithmetic with three real products per complex
+// MAC (the k dimension of an m8n8k4 step is 4 complex rows):
+//   P1 = S_r^T T_r,  P2 = S_i^T T_i,  P3 = (S_r - S_i)^T (T_r + T_i)
+//   Re G = P1 + P2,  Im G = P3 - P1 + P2       (conj(S)^T T; 25% fewer MMAs than 4 real products)
 // CTA output block BM x BN = (WARPS_M*WM*8) x (WARPS_N*WN*8) complex; each warp owns WM x WN m8n8
 // tiles.  Rows stream through a STAGES-deep cp.async pipeline in chunks of KC complex rows.
 // Split-K over rows; partials reduced in a fixed order (deterministic).
@@ -12,7 +13,7 @@ template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
 struct GramCfg {
   static constexpr int BM = WARPS_M * WM * 8, BN = WARPS_N * WN * 8;
   static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
-  static constexpr int PITCH = 2 * KC + 4;  // doubles per column: 8 mod 32 words -> conflict-free fragments
+  static constexpr int PITCH = 2 * KC + 8;  // doubles per column, 8 mod 16: 16-B fragment loads conflict-free
   static constexpr size_t SMEM = (size_t)STAGES * (BM + BN) * PITCH * sizeof(double);
 };
 
@@ -31,11 +32,13 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
   const long long r0 = (long long)blockIdx.y * rows_per_split;
   const long long r1 = min(len, r0 + rows_per_split);
 
-  double accR[WM][WN][2], accI[WM][WN][2];
+  double p1[WM][WN][2], p2[WM][WN][2], p3[WM][WN][2];
 #pragma unroll
   for (int i = 0; i < WM; i++)
 #pragma unroll
-    for (int j = 0; j < WN; j++) accR[i][j][0] = accR[i][j][1] = accI[i][j][0] = accI[i][j][1] = 0.0;
+    for (int j = 0; j < WN; j++)
+#pragma unroll
+      for (int e = 0; e < 2; e++) p1[i][j][e] = p2[i][j][e] = p3[i][j][e] = 0.0;
 
   const cplx* dummy = S.p[0];
   auto load_chunk = [&](int stage, long long rbase) {
@@ -80,24 +83,31 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
       const int st = ch % STAGES;
       const double* A = As + st * BM * PITCH;
       const double* B = Bs + st * BN * PITCH;
-#pragma unroll 4
-      for (int s4 = 0; s4 < 2 * KC / 4; s4++) {
-        const int kk = 4 * s4 + (lane & 3);
-        double a[WM], b[WN], bi[WN];
+#pragma unroll 2
+      for (int s4 = 0; s4 < KC / 4; s4++) {
+        const int kk = 2 * (4 * s4 + (lane & 3));  // complex row 4 s4 + (lane & 3), interleaved doubles
+        double ar[WM], ai[WM], ad[WM], br[WN], bi[WN], bs[WN];
 #pragma unroll
-        for (int mt = 0; mt < WM; mt++) a[mt] = A[(wm * WM * 8 + mt * 8 + (lane >> 2)) * PITCH + kk];
+        for (int mt = 0; mt < WM; mt++) {
+          const double2 v = *reinterpret_cast<const double2*>(&A[(wm * WM * 8 + mt * 8 + (lane >> 2)) * PITCH + kk]);
+          ar[mt] = v.x;
+          ai[mt] = v.y;
+          ad[mt] = v.x - v.y;
+        }
 #pragma unroll
         for (int nt = 0; nt < WN; nt++) {
-          b[nt] = B[(wn * WN * 8 + nt * 8 + (lane >> 2)) * PITCH + kk];
-          const double bx = __shfl_xor_sync(0xffffffffu, b[nt], 1);
-          bi[nt] = (lane & 1) ? -bx : bx;
+          const double2 v = *reinterpret_cast<const double2*>(&B[(wn * WN * 8 + nt * 8 + (lane >> 2)) * PITCH + kk]);
+          br[nt] = v.x;
+          bi[nt] = v.y;
+          bs[nt] = v.x + v.y;
         }
 #pragma unroll
         for (int mt = 0; mt < WM; mt++)
 #pragma unroll
           for (int nt = 0; nt < WN; nt++) {
-            dmma(accR[mt][nt][0], accR[mt][nt][1], a[mt], b[nt]);
-            dmma(accI[mt][nt][0], accI[mt][nt][1], a[mt], bi[nt]);
+            dmma(p1[mt][nt][0], p1[mt][nt][1], ar[mt], br[nt]);
+            dmma(p2[mt][nt][0], p2[mt][nt][1], ai[mt], bi[nt]);
+            dmma(p3[mt][nt][0], p3[mt][nt][1], ad[mt], bs[nt]);
           }
       }
     }
@@ -114,7 +124,10 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
       for (int e = 0; e < 2; e++) {
         const int m = m0 + wm * WM * 8 + mt * 8 + (lane >> 2);
         const int n = n0 + wn * WN * 8 + nt * 8 + 2 * (lane & 3) + e;
-        if (m < p && n < q) out[(size_t)n * p + m] = mk(accR[mt][nt][e], accI[mt][nt][e]);
+        if (m < p && n < q) {
+          const double re = p1[mt][nt][e] + p2[mt][nt][e];
+          out[(size_t)n * p + m] = mk(re, p3[mt][nt][e] - p1[mt][nt][e] + p2[mt][nt][e]);
+        }
       }
 }
 

@@ -28,6 +28,7 @@ struct PassArgsH {
   const cplx* ktab;  // symbol pieces, see pointwise.cu
   double gamma;
   double scale;
+  int z0 = 0, nz = 0;  // x/y passes: restrict to z-planes [z0, z0+nz) (nz = 0: all)
 };
 
 // FFT passes ------------------------------------------------------------------------------
@@ -41,7 +42,7 @@ cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& i
 // fused x-inverse DFT + M_eps + x-forward DFT (media with eps_13 = eps_23 = 0 in CrossDoF mode; any
 // Diagonal/Trivial medium): in -> out (must differ), output scaled by `scale`.
 cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
-                       const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st);
+                       const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st);
 
 // pointwise ---------------------------------------------------------------------------------
 void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t st);
@@ -53,6 +54,7 @@ int resid_grid(int n);
 void launch_resid(const ColPtrs& X, const ColPtrs& AX, const MutColPtrs& W, const double* lam, int b, int n,
                   const cplx* kt, double gamma, double thr, int deflate0, double* partial, double* norms,
                   cudaStream_t st);
+void launch_reduce_partial(const double* partial, int nb, int ncols, double* norms, cudaStream_t st);
 void launch_randn(const MutColPtrs& X, int ncols, long long len, unsigned long long seed, int deflate_stride,
                   double scale, cudaStream_t st);
 // plane-wave start block: per-CTA PW_T smallest |kappa|^2 (pw_grid() CTAs), then a host-built scatter
@@ -78,6 +80,15 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st);
+
+// A-image update fused with the next residual (update_resid.cu): Y1/Y2 as in launch_update (r <= 32),
+// then R = Y2 - Xn diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if
+// deflate0), per-CTA |R_c|^2, |Xn_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  Returns the grid
+// (<= max_grid) for launch_reduce_partial.
+int launch_update_resid(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
+                        const MutColPtrs& Y2, const ColPtrs& Xn, const MutColPtrs& W, const double* lam, int n,
+                        const cplx* kt, double gamma, double thr, int deflate0, double* partial, int max_grid,
+                        cudaStream_t st);
 
 // Rayleigh-Ritz ------------------------------------------------------------------------------
 // G = [G_M | G_A] (p x 2p, column-major ld p).  Outputs C (p x nb, ld p), lambda (nb), info[0] = rank,

@@ -92,6 +92,8 @@ struct pc_ctx {
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
+  int fuse_resid = 0;          // residual + K_P^{-1} fused into the A-image update (update_resid.cu)
+  double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
   DevBuf pwbuf;
@@ -375,6 +377,8 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "gram_refresh") c->gram_refresh = (int)v;
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
+  else if (k == "fuse_resid") c->fuse_resid = (int)v;
+  else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
@@ -438,12 +442,14 @@ static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
 // apply
 // ------------------------------------------------------------------------------------------
 static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
-                    const ColPtrs& xh, int nc, double scale, cudaStream_t st) {
+                    const ColPtrs& xh, int nc, double scale, cudaStream_t st, int z0 = 0, int nz = 0) {
   PassArgsH a;
   a.tw = c->d_tw;
   a.ktab = c->d_ktab;
   a.gamma = c->cur_gamma;
   a.scale = scale;
+  a.z0 = z0;
+  a.nz = nz;
   cudaError_t e = launch_fft_pass(c->n, axis, dir, kind, in, out, xh, nc, a, st);
   if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("fft pass: ") + cudaGetErrorString(e));
   return PC_OK;
@@ -473,18 +479,48 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
   const bool plane_local = c->fuse_xex && (c->eps_mode != PC_EPS_CROSSDOF || (!c->ec.has[1] && !c->ec.has[2]));
   if (plane_local) {
-    {
-      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
-      CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
+    // Middle passes (y-inverse, x-inverse + M_eps + x-forward, y-forward) in L2-sized chunks of
+    // (column, z-planes): the chunk written by one pass is re-read by the next while it is still in
+    // the 126 MB L2, so HBM only sees the first read of u and the final write-back of s.
+    const double chunk_bytes = c->chunk_mb * 1048576.0;
+    const double plane_bytes = 3.0 * n * n * sizeof(cplx);  // one z-plane, 3 components, one column
+    int nzc = n;
+    if (c->chunk_mb > 0) {
+      nzc = (int)std::max(1.0, std::floor(chunk_bytes / plane_bytes));
+      while (nzc < n && n % nzc) nzc--;  // divisor of n
+      nzc = std::min(nzc, n);
     }
-    {
-      Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 100.0 * pts, 96.0 * pts);
-      cudaError_t e = launch_xex(n, c->eps_mode, Yc, WS, nc, c->d_mask, c->ec, c->d_tw, 1.0, st);
-      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
-    }
-    {
-      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
-      CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
+    const int ccols = (nzc == n && c->chunk_mb > 0)
+                          ? std::max(1, std::min(nc, (int)std::floor(chunk_bytes / (plane_bytes * n))))
+                          : (c->chunk_mb > 0 ? 1 : nc);
+    for (int j0 = 0; j0 < nc; j0 += ccols) {
+      const int cn = std::min(ccols, nc - j0);
+      ColPtrs Ys, Ws;
+      MutColPtrs Ym, Wm;
+      for (int j = 0; j < cn; j++) {
+        Ys.p[j] = Yc.p[j0 + j];
+        Ws.p[j] = Wc.p[j0 + j];
+        Ym.p[j] = Y.p[j0 + j];
+        Wm.p[j] = WS.p[j0 + j];
+      }
+      for (int z0 = 0; z0 < n; z0 += nzc) {
+        const int nz = (nzc == n) ? 0 : nzc;
+        const double cp = (double)cn * n * n * (nz ? nz : n);
+        const double cfl = 15.0 * std::log2((double)n) * cp;
+        {
+          Prof p(c, PC_STAT_FFT_MID, st, 1, cfl, 96.0 * cp);
+          CHK(fft_pass(c, 1, +1, 0, Ys, Ym, none, cn, 1.0, st, z0, nz));
+        }
+        {
+          Prof p(c, PC_STAT_EPS, st, 1, 2 * cfl + 100.0 * cp, 96.0 * cp);
+          cudaError_t e = launch_xex(n, c->eps_mode, Ys, Wm, cn, c->d_mask, c->ec, c->d_tw, 1.0, z0, nz, st);
+          if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
+        }
+        {
+          Prof p(c, PC_STAT_FFT_MID, st, 1, cfl, 96.0 * cp);
+          CHK(fft_pass(c, 1, -1, 0, Ws, Wm, none, cn, 1.0, st, z0, nz));
+        }
+      }
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 40.0 * pts, 144.0 * pts);
@@ -884,12 +920,12 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   std::vector<double> res(b, 0.0);
   c->hist.clear();
   c->hist_b = b;
-  bool haveP = false;
+  bool haveP = false, resid_ready = false;
   int it = 0, conv = 0;
   for (;; it++) {
     // residuals of every column; W = K_P^{-1} R only for the columns that can receive a search direction
-    {
-      const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
+    const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
+    if (!resid_ready) {
       Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + nw));
       ColPtrs X, AX;
       MutColPtrs W;
@@ -964,7 +1000,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     }
     // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images
     {
-      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b, 2 * 16.0 * len * (p + 2 * b));
+      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + (c->fuse_resid ? 84.0 * c->n3 * b : 0.0),
+              2 * 16.0 * len * (p + 2 * b) + (c->fuse_resid ? 16.0 * len * (b + nw) : 0.0));
       ColPtrs S;
       MutColPtrs Y1, Y2;
       ccols(sX, all, S, 0);
@@ -978,7 +1015,22 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (haveP) ccols(sAP, act, S, b + na);
       mcols(sAPn, all, Y1, 0);
       mcols(sAXn, all, Y2, 0);
-      launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
+      if (c->fuse_resid) {
+        // A-image update + next residual R = AX' - X' Lambda', W = K_P^{-1} R (WW is free again: the
+        // S-update above consumed it), |R|^2 and |X'|^2 partials
+        ColPtrs Xn;
+        MutColPtrs W;
+        ccols(sXn, all, Xn, 0);
+        mcols(WW, all, W, 0);
+        for (int j = nw; j < b; j++) W.p[j] = nullptr;
+        const int g = launch_update_resid(S, p, dC, p, b, b, &Y1, Y2, Xn, W, dLam, c->n, c->d_ktab, c->cur_gamma,
+                                          c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+        launch_reduce_partial(dPart, g, b, dNorm, st);
+        c->launches += 1;
+        resid_ready = true;
+      } else {
+        launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
+      }
     }
     std::swap(sX, sXn);
     std::swap(sAX, sAXn);

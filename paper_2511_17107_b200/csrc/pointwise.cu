@@ -30,24 +30,7 @@ void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t 
   ktab_kernel<<<(tot + 127) / 128, 128, 0, st>>>(ktab, tw, n, s);
 }
 
-DEV void kappa_at(const cplx* __restrict__ kt, int n, int m1, int m2, int m3, cplx& k1, cplx& k2, cplx& k3) {
-  k1 = ldg(kt + 0 * n + m1) + ldg(kt + 1 * n + m2) + ldg(kt + 2 * n + m3);
-  k2 = ldg(kt + 3 * n + m1) + ldg(kt + 4 * n + m2) + ldg(kt + 5 * n + m3);
-  k3 = ldg(kt + 6 * n + m1) + ldg(kt + 7 * n + m2) + ldg(kt + 8 * n + m3);
-}
-
-// x = K_P^{-1} r = r/|k|^2 - (gamma-1)/(gamma |k|^4) conj(k) (k^T r); pass-through if |k|^2 <= thr
-DEV void kp_inv(cplx k1, cplx k2, cplx k3, double gamma, double thr, cplx& r1, cplx& r2, cplx& r3) {
-  double k2n = abs2(k1) + abs2(k2) + abs2(k3);
-  if (k2n <= thr) return;
-  double inv = 1.0 / k2n;
-  cplx kr = cmul(k1, r1) + cmul(k2, r2) + cmul(k3, r3);
-  double f = (gamma - 1.0) / (gamma * k2n * k2n);
-  kr = mk(f * kr.x, f * kr.y);
-  r1 = inv * r1 - cmul(conjg(k1), kr);
-  r2 = inv * r2 - cmul(conjg(k2), kr);
-  r3 = inv * r3 - cmul(conjg(k3), kr);
-}
+#include "kp.cuh"  // kappa_at, kp_inv
 
 __global__ void precond_kernel(ColPtrs in, MutColPtrs out, int n, const cplx* __restrict__ kt, double gamma,
                                double thr) {
@@ -273,6 +256,10 @@ void launch_resid(const ColPtrs& X, const ColPtrs& AX, const MutColPtrs& W, cons
   int gx = resid_grid(n);
   resid_kernel<<<dim3(gx, b), 256, 0, st>>>(X, AX, W, lam, n, kt, gamma, thr, deflate0, partial);
   reduce_partial_kernel<<<b, 256, 0, st>>>(partial, gx, b, norms);
+}
+
+void launch_reduce_partial(const double* partial, int nb, int ncols, double* norms, cudaStream_t st) {
+  reduce_partial_kernel<<<ncols, 256, 0, st>>>(partial, nb, ncols, norms);
 }
 
 // ------------------------------------------------------------------------------------------

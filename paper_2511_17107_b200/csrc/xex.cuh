@@ -62,7 +62,7 @@ struct XexCfg {
 template <int N, int MODE>
 __global__ void __launch_bounds__(XexCfg<N>::NT, 3)
 xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
-           double scale) {
+           double scale, int zoff) {
   using Cfg = XexCfg<N>;
   constexpr int TP = Cfg::TP, RP = Cfg::RP, NP1 = Cfg::NP1, NT = Cfg::NT, PPT = Cfg::PPT;
   constexpr int N3 = N * N * N;
@@ -71,7 +71,7 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   cplx* tw = s + 3 * RP * NP1;
   uint8_t* mk8 = reinterpret_cast<uint8_t*>(tw + N);  // [row][x]
   const int tid = threadIdx.x;
-  const int z = blockIdx.x / (N / TP), y0 = (blockIdx.x % (N / TP)) * TP;
+  const int z = zoff + blockIdx.x / (N / TP), y0 = (blockIdx.x % (N / TP)) * TP;
   const int col = blockIdx.y;
   const cplx* gin = in.p[col];
   cplx* gout = out.p[col];
