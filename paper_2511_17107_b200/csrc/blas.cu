@@ -43,25 +43,34 @@ void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx*
 //         phase 2  acc += sum_{m in [0, split)} S[:, m] C[m, :] -> Y2 (+ Add)
 // r <= 8 NT output columns.  CTA = 8 warps x 8 rows = 64-row tiles, persistent over row tiles with a
 // 2-stage cp.async pipeline (tile t+1 streams in while tile t is multiplied).  S tile in smem as
-// [m][row] (as streamed from HBM, conflict-free cp.async) with row pitch RP = 4 mod 8 complex (conflict-free
-// A fragments); C as [c][m] with pitch PS = 2 mod 8.
+// [m][row] (as streamed from HBM, conflict-free cp.async) with row pitch RP = 2 mod 8 complex; C as
+// [c][m] with pitch PS = 4 mod 8 (conflict-free 16-B fragment loads).  Complex products with three real
+// MMAs per m8n8k4 step of 4 complex m:  P1 = S_r C_r, P2 = S_i C_i, P3 = (S_r + S_i)(C_r + C_i),
+// Re = P1 - P2, Im = P3 - P1 - P2.
 // ------------------------------------------------------------------------------------------
-constexpr int U_ROWS = 64, U_THREADS = 256;
+static int g_update_warps = 4;  // CTA = g_update_warps x 8 rows (pc_set_option "update_warps": 4, 8, 16)
+void set_update_warps(int w) { g_update_warps = (w == 8 || w == 16) ? w : 4; }
 
 HD int pitch2mod8(int p) {
   int x = p + 1;
   while ((x & 7) != 2) x++;
   return x;
 }
+HD int pitch4mod8(int p) {
+  int x = p;
+  while ((x & 7) != 4) x++;
+  return x;
+}
 
-template <int NT>
-__global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, const cplx* __restrict__ C, int ldc,
+template <int NT, int WARPS>
+__global__ void __launch_bounds__(32 * WARPS) update_kernel(ColPtrs S, int p, const cplx* __restrict__ C, int ldc,
                                                            int r, int split, MutColPtrs Y1, int has_y1, MutColPtrs Y2,
                                                            ColPtrs Add, int has_add, long long len) {
   extern __shared__ __align__(16) double usm[];
-  const int pe = (p + 1) & ~1;  // even number of S columns (k' multiple of 4)
-  const int PS = pitch2mod8(pe);
-  constexpr int RP = U_ROWS + 4;             // 4 mod 8
+  const int pe = (p + 3) & ~3;  // S columns padded to the k = 4 complex step
+  const int PS = pitch4mod8(pe);
+  constexpr int U_ROWS = 8 * WARPS, U_THREADS = 32 * WARPS;
+  constexpr int RP = U_ROWS + 2;  // 2 mod 8
   cplx* Ss = reinterpret_cast<cplx*>(usm);   // [2][pe][RP]
   cplx* Cs = Ss + 2 * pe * RP;               // [NT*8][PS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -95,26 +104,26 @@ __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, con
     }
     __syncthreads();
     const long long rbase = t * U_ROWS;
-    double accR[NT][2], accI[NT][2];
+    double p1[NT][2], p2[NT][2], p3[NT][2];
 #pragma unroll
-    for (int nt = 0; nt < NT; nt++) accR[nt][0] = accR[nt][1] = accI[nt][0] = accI[nt][1] = 0.0;
-    const double* Sd = reinterpret_cast<const double*>(Ss + st * pe * RP);
+    for (int nt = 0; nt < NT; nt++) p1[nt][0] = p1[nt][1] = p2[nt][0] = p2[nt][1] = p3[nt][0] = p3[nt][1] = 0.0;
+    const cplx* Sc = Ss + st * pe * RP;
     const int arow = warp * 8 + (lane >> 2);
 
     auto kloop = [&](int mlo, int mhi) {  // contributions of S columns m in [mlo, mhi)
 #pragma unroll 2
-      for (int m2 = mlo & ~1; m2 < mhi; m2 += 2) {  // one k4 step = 2 complex m
-        const int mm = m2 + ((lane & 3) >> 1);
-        const double a = Sd[2 * (mm * RP + arow) + (lane & 1)];
+      for (int m4 = mlo & ~3; m4 < mhi; m4 += 4) {  // one k4 step = 4 complex m
+        const int mm = m4 + (lane & 3);
         const bool in = (mm >= mlo) && (mm < mhi);
+        const cplx a = Sc[mm * RP + arow];
+        const double as = a.x + a.y;
 #pragma unroll
         for (int nt = 0; nt < NT; nt++) {
           cplx cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
           if (!in) cv = mk(0, 0);
-          const double br = (lane & 1) ? -cv.y : cv.x;
-          const double bi = (lane & 1) ? cv.x : cv.y;
-          dmma(accR[nt][0], accR[nt][1], a, br);
-          dmma(accI[nt][0], accI[nt][1], a, bi);
+          dmma(p1[nt][0], p1[nt][1], a.x, cv.x);
+          dmma(p2[nt][0], p2[nt][1], a.y, cv.y);
+          dmma(p3[nt][0], p3[nt][1], as, cv.x + cv.y);
         }
       }
     };
@@ -126,8 +135,8 @@ __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, con
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           int c = nt * 8 + 2 * (lane & 3) + e;
-          if (c < r) {
-            cplx v = mk(accR[nt][e], accI[nt][e]);
+          if (c < r && Y.p[c]) {
+            cplx v = mk(p1[nt][e] - p2[nt][e], p3[nt][e] - p1[nt][e] - p2[nt][e]);
             if (add) v = v + Add.p[c][row];
             Y.p[c][row] = v;
           }
@@ -141,28 +150,38 @@ __global__ void __launch_bounds__(U_THREADS) update_kernel(ColPtrs S, int p, con
   }
 }
 
-template <int NT>
+template <int NT, int WARPS>
 static void run_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                        const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
-  const int pe = (p + 1) & ~1, ps = pitch2mod8(pe);
-  const size_t smem = (size_t)(2 * pe * (U_ROWS + 4) + NT * 8 * ps) * sizeof(cplx);
+  constexpr int U_ROWS = 8 * WARPS;
+  const int pe = (p + 3) & ~3, ps = pitch4mod8(pe);
+  const size_t smem = (size_t)(2 * pe * (U_ROWS + 2) + NT * 8 * ps) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(update_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
+    cudaFuncSetAttribute(update_kernel<NT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
     attr = true;
   }
   const long long ntiles = (len + U_ROWS - 1) / U_ROWS;
-  const int occ = std::max(1, std::min(3, (int)((227 * 1024) / (smem + 1024))));
+  const int occ = std::max(1, std::min(64 / WARPS, (int)((227 * 1024) / (smem + 1024))));
   const int grid = (int)std::min<long long>(ntiles, 148LL * occ);
   MutColPtrs y1 = Y1 ? *Y1 : MutColPtrs{};
   ColPtrs ad = add ? *add : ColPtrs{};
-  update_kernel<NT><<<grid, U_THREADS, smem, st>>>(S, p, C, ldc, r, split, y1, Y1 ? 1 : 0, Y2, ad, add ? 1 : 0, len);
+  update_kernel<NT, WARPS><<<grid, 32 * WARPS, smem, st>>>(S, p, C, ldc, r, split, y1, Y1 ? 1 : 0, Y2, ad,
+                                                           add ? 1 : 0, len);
+}
+
+template <int WARPS>
+static void launch_update_w(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
+                            const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
+  if (r <= 8) run_update<1, WARPS>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else if (r <= 16) run_update<2, WARPS>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else if (r <= 24) run_update<3, WARPS>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else run_update<4, WARPS>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
 }
 
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
-  if (r <= 8) run_update<1>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
-  else if (r <= 16) run_update<2>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
-  else if (r <= 24) run_update<3>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
-  else run_update<4>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  if (g_update_warps == 4) launch_update_w<4>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else if (g_update_warps == 16) launch_update_w<16>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  else launch_update_w<8>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
 }

@@ -76,8 +76,9 @@ void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx*
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                  cudaStream_t st);
 // Block update (r <= 32 output columns, C column-major ld = ldc):
-//   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr)
+//   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr; columns with Y1->p[c] == nullptr skipped)
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])
+void set_update_warps(int w);  // tuning knob (4, 8 or 16 warps per update CTA)
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st);
 

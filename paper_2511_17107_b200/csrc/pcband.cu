@@ -378,6 +378,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
+  else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
@@ -1001,7 +1002,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images
     {
       Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + (c->fuse_resid ? 84.0 * c->n3 * b : 0.0),
-              2 * 16.0 * len * (p + 2 * b) + (c->fuse_resid ? 16.0 * len * (b + nw) : 0.0));
+              2 * 16.0 * len * (p + b + nw) + (c->fuse_resid ? 16.0 * len * (b + nw) : 0.0));
       ColPtrs S;
       MutColPtrs Y1, Y2;
       ccols(sX, all, S, 0);
@@ -1009,12 +1010,14 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (haveP) ccols(sP, act, S, b + na);
       mcols(sPn, all, Y1, 0);
       mcols(sXn, all, Y2, 0);
+      for (int j = nw; j < b; j++) Y1.p[j] = nullptr;  // columns that never get W never use P
       launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
       ccols(sAX, all, S, 0);
       ccols(AWW, act, S, b);
       if (haveP) ccols(sAP, act, S, b + na);
       mcols(sAPn, all, Y1, 0);
       mcols(sAXn, all, Y2, 0);
+      for (int j = nw; j < b; j++) Y1.p[j] = nullptr;
       if (c->fuse_resid) {
         // A-image update + next residual R = AX' - X' Lambda', W = K_P^{-1} R (WW is free again: the
         // S-update above consumed it), |R|^2 and |X'|^2 partials

@@ -118,7 +118,7 @@ __global__ void __launch_bounds__(UR_THREADS) update_resid_kernel(
 #pragma unroll
         for (int e = 0; e < 2; e++) {
           const int c = nt * 8 + 2 * (lane & 3) + e;
-          if (c < r) {
+          if (c < r && Y.p[c]) {
 #pragma unroll
             for (int s = 0; s < 3; s++) Y.p[c][(long long)s * n3 + mode] = mk(accR[s][i][e], accI[s][i][e]);
           }
