@@ -186,7 +186,10 @@ def workload_config(W, args):
                         f"tol={args.tol:g}, k-path {len(W.kpoints())} points",
             "n": W.n, "nev": W.nev, "block": W.nev + 5, "tol": args.tol, "lattice": W.lattice,
             "geometry": W.geometry, "eps_mode": "crossdof",
-            "l2": "no flush: per-k working set ~15 GB >> 126 MB L2"}
+            "l2": "no flush: per-k working set ~15 GB >> 126 MB L2",
+            "start": ("warm: each context solves a contiguous k stretch, k_i started from k_(i-1)'s Ritz block "
+                      "(SURVEY f2, not the paper's protocol)") if getattr(args, "warm_start", False)
+            else "cold: seeded plane-wave + Gaussian start block per k"}
 
 
 # ------------------------------------------------------------------------------------------
@@ -207,6 +210,9 @@ def main():
     ap.add_argument("--guard", type=int, default=None, help="LOBPCG guard columns (block = nev + guard)")
     ap.add_argument("--streams", type=int, default=2, help="concurrent k-point solves per GPU (contexts)")
     ap.add_argument("--w-guard", type=int, default=None, help="guard columns that get search directions")
+    ap.add_argument("--warm-start", action="store_true",
+                    help="path continuation: contiguous k stretches per context, each k started from the "
+                         "previous k's Ritz block (SURVEY f2; not the paper's cold start, reported separately)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -244,9 +250,13 @@ def main():
     ctx = ctxs[0]
 
     def kidx(s):
+        if args.warm_start:  # contiguous stretch per rank
+            return (rank * (args.warmup + args.steps + len(ctxs)) + s) % nk
         return (rank + world * s) % nk
 
     def run(idx_list):
+        if args.warm_start:
+            return bands.solve_warm(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
         if len(ctxs) == 1:
             return bands.solve_local(ctx, kp, idx_list, W.nev, args.tol, args.maxit, 0)
         return bands.solve_concurrent(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
@@ -327,7 +337,31 @@ def main():
              "design_bytes_per_point_col": 720, "design_gbs": design_gbs,
              "kernels": {k: {"ms_per_apply": v["ms"] / reps, "gbs": (v["bytes"] / v["ms"] / 1e6) if v["ms"] else None}
                          for k, v in astats.items() if isinstance(v, dict) and v["count"]}}
+    # library composition of the same apply (cuFFT via torch.fft + elementwise torch kernels: the
+    # paper's GPU recipe on this GPU); same input block, agreement checked
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        from library_apply import LibraryApply
+        lib_ap = LibraryApply(W.n, A, kk, eps1, masks, api.pc_gamma(ctx, kk), dev)
+        Yl = lib_ap(X)
+        rel = float(torch.linalg.vector_norm(Yl - Y) / torch.linalg.vector_norm(Y))
+        torch.cuda.synchronize()
+        l0, l1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        l0.record()
+        for _ in range(reps):
+            Yl = lib_ap(X)
+        l1.record()
+        torch.cuda.synchronize()
+        lib_ms = l0.elapsed_time(l1) / reps
+        apply["library_baseline"] = {"what": "torch.fft (cuFFT Z2Z 3-D, batch 3 x cols) + torch elementwise/roll "
+                                             "kernels for kappa products and the CrossDoF stencil",
+                                     "ms": lib_ms, "alg_gbs": 336.0 * pts / (lib_ms * 1e6),
+                                     "speedup_fused": lib_ms / apply_ms, "rel_diff_vs_pc_apply": rel}
+        del Yl, lib_ap
+    except Exception as ex:  # pragma: no cover - report, never fall back
+        apply["library_baseline"] = {"error": str(ex)[:200]}
     del X, Y
+    torch.cuda.empty_cache()
 
     # ---- roofline of the dominant kernel class.  Inside the timed region the concurrent contexts'
     # kernels interleave, so a class's event time there includes the other streams' kernels; the

@@ -173,6 +173,16 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  X^H X = I, X^H A X = Lambda (default 16; 0 = never)
  *   "p_restart"    1 (default): drop the P block when the basis is numerically rank deficient
  *   "verbose"      1: per-iteration residuals on stderr
+ *   "warm_start"   1: start each k-point (k != 0) from the Ritz block of the previous pc_bands
+ *                  k-point solved on this context (path continuation, not in the
+ *                  paper); 0 (default): cold start.  Setting the option forgets the stored block.
+ *   "w_guard"      guard columns that receive a search direction W (default 0: only the nev
+ *                  wanted columns; -1: all b columns)
+ *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
+ *                  Diagonal/Trivial mode); 0: 7-pass pipeline with the standalone stencil
+ *   "fuse_resid"   1: residual + K_P^{-1} fused into the A-image block update; 0 (default): separate
+ *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)
+ *   "update_warps" 4 (default), 8 or 16 warps per block-update CTA (process-wide tuning knob)
  */
 int pc_set_option(pc_ctx *ctx, const char *key, double value);
 

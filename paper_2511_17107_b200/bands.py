@@ -19,6 +19,14 @@ def shard(nk: int, world: int, rank: int) -> list:
     return list(range(rank, nk, world))
 
 
+def shard_contiguous(nk: int, world: int, rank: int) -> list:
+    """Global k indices owned by `rank` as one contiguous stretch of the path (warm-start mode:
+    neighbouring k-points stay on one rank)."""
+    base, extra = divmod(nk, world)
+    lo = rank * base + min(rank, extra)
+    return list(range(lo, lo + base + (1 if rank < extra else 0)))
+
+
 def local_capacity(nk: int, world: int) -> int:
     return (nk + world - 1) // world
 
@@ -70,6 +78,42 @@ def solve_concurrent(ctxs, kpts: np.ndarray, idx: list, nev: int, tol: float, ma
             errors.append(ex)
 
     threads = [threading.Thread(target=worker, args=(c,)) for c in ctxs]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    if errors:
+        raise errors[0]
+    return om, rs, it, stt
+
+
+def solve_warm(ctxs, kpts: np.ndarray, idx: list, nev: int, tol: float, maxit: int, seed: int):
+    """Warm-started path continuation (not in the paper): idx is split into
+    len(ctxs) contiguous stretches, each solved in path order on its own context with the option
+    warm_start = 1 (the start block of k_i is the Ritz block of k_{i-1}; k = 0 exactly still starts
+    cold).  Contexts run concurrently, one host thread each."""
+    import threading
+    from . import api
+    om = np.zeros((len(idx), nev))
+    rs = np.zeros((len(idx), nev))
+    it = np.zeros(len(idx), dtype=np.int64)
+    stt = np.zeros(len(idx), dtype=np.int64)
+    parts = [shard_contiguous(len(idx), len(ctxs), r) for r in range(len(ctxs))]
+    errors = []
+
+    def worker(ctx, ts):
+        try:
+            api.pc_set_option(ctx, "warm_start", 1)
+            for t in ts:
+                g = idx[t]
+                api.pc_set_option(ctx, "kindex_offset", g)
+                r = api.pc_bands(ctx, kpts[g:g + 1], nev=nev, tol=tol, maxit=maxit, seed=seed)
+                om[t], rs[t], it[t], stt[t] = r["omega2"][0], r["resid"][0], r["iters"][0], r["status"][0]
+            api.pc_set_option(ctx, "warm_start", 0)
+        except Exception as ex:  # pragma: no cover - surfaced below
+            errors.append(ex)
+
+    threads = [threading.Thread(target=worker, args=(c, ts)) for c, ts in zip(ctxs, parts)]
     for th in threads:
         th.start()
     for th in threads:

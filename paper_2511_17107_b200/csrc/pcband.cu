@@ -96,6 +96,8 @@ struct pc_ctx {
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
+  int warm_start = 0;          // 1: start from the previous k-point's Ritz vectors (same context, k != 0)
+  int have_prev = 0, prev_slot = 0, prev_b = 0;
   DevBuf pwbuf;
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
@@ -373,6 +375,10 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "verbose") c->verbose = (int)v;
   else if (k == "p_restart") c->p_restart = (int)v;
   else if (k == "start") c->start_mode = (int)v;
+  else if (k == "warm_start") {
+    c->warm_start = (int)v;
+    c->have_prev = 0;
+  }
   else if (k == "sticky_lock") c->sticky_lock = (int)v;
   else if (k == "gram_refresh") c->gram_refresh = (int)v;
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
@@ -882,7 +888,14 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   // b/2 Fourier modes with the smallest |kappa(m)|^2 -- the eigenvectors of K_P, i.e.
   // of the vacuum operator -- plus a small seeded Gaussian admixture (reading R14: the paper does
   // not state its start block).
-  {
+  // warm start (not in the paper): the previous k-point's Ritz vectors on this context
+  const bool warm = c->warm_start && c->have_prev && c->prev_b == b && !deflate;
+  c->have_prev = 0;  // set again only by a completed solve
+  if (warm) {
+    Prof pf(c, PC_STAT_OTHER, st, 1, 0.0, 32.0 * len * b);
+    if (c->prev_slot != sX)
+      CU(cudaMemcpyAsync(col(sX, 0), col(c->prev_slot, 0), (size_t)b * colb, cudaMemcpyDeviceToDevice, st));
+  } else {
     const bool pw = c->start_mode == 1;
     const double noise = pw ? c->start_noise / std::sqrt((double)len) : 1.0;
     Prof pf(c, PC_STAT_OTHER, st, pw ? 3 : 1, 0.0, 16.0 * len * b);
@@ -1042,6 +1055,9 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     haveP = true;
   }
   // outputs
+  c->have_prev = 1;
+  c->prev_slot = sX;
+  c->prev_b = b;
   cudaMemcpyAsync(hN + 2 * b, dLam, b * sizeof(double), cudaMemcpyDeviceToHost, st);
   if (evec_out) {
     ColPtrs X;

@@ -188,3 +188,25 @@ def test_bands_eigenvectors(api):
     res = np.linalg.norm(AV - r["omega2"][0][:, None] * V, axis=1)
     assert np.allclose(np.linalg.norm(V, axis=1), 1.0, atol=1e-12)
     assert res.max() <= 1e-8
+
+
+def test_bands_warm_start_path_continuation(api):
+    """Warm start: same eigenvalues as cold starts (both to TOL, compared at 1e-8
+    relative against the dense oracle at n=8), path includes Gamma (cold there), and fewer total
+    iterations than the cold path."""
+    from paper_2511_17107_b200 import bands
+    A = synth.lattice("fcc")
+    n = 8
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("random", A, n, seed=21)
+    kp = synth.kpath("fcc", 4)[6:16]  # U -> L -> Gamma -> ... (contains k = 0)
+    ctx = api.pc_create(A, n, e, masks)
+    cold = bands.solve_local(ctx, kp, list(range(len(kp))), 6, TOL, 500, 0)
+    warm = bands.solve_warm([ctx], kp, list(range(len(kp))), 6, TOL, 500, 0)
+    assert (cold[3] == 0).all() and (warm[3] == 0).all()
+    for i, k in enumerate(kp):
+        op = O.PenalizedOperator(n, k, A, e, masks)
+        ref = O.eigs_dense(op, 6)
+        assert rel(warm[0][i], ref) <= 1e-8
+        assert rel(cold[0][i], ref) <= 1e-8
+    assert warm[2].sum() < cold[2].sum()

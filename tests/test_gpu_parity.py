@@ -230,3 +230,28 @@ def test_fused_xex_pipeline_matches_unfused(api, eps, mode, n):
     if n <= 16:
         op = O.PenalizedOperator(n, np.array(k), A, e, masks, mode)
         assert relerr_cols(Y1.cpu().numpy(), op.apply_fourier(X.cpu().numpy())) <= 1e-12
+
+
+@pytest.mark.parametrize("eps,n", [("sdd", 8), ("pc", 12), ("pc", 64)])
+def test_library_composition_baseline_matches(api, eps, n):
+    """The cuFFT + elementwise comparison arm (tools/library_apply.py, timed by bench.py) computes the
+    same operator: against the oracle at small n and against pc_apply at n = 64."""
+    import os
+    import sys
+    sys.path.insert(0, os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "tools"))
+    from library_apply import LibraryApply
+    A = synth.lattice("fcc")
+    e = _eps(eps)
+    masks = synth.make_masks("random" if n <= 12 else "fcc_diamond", A, n, seed=5)
+    k = np.array([0.7, -PI / 3, 1.9])
+    ctx = api.pc_create(A, n, e, masks)
+    X = torch.randn(2, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    Y = torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y)
+    L = LibraryApply(n, A, k, e, masks, api.pc_gamma(ctx, k), "cuda")
+    Yl = L(X)
+    err = (torch.linalg.vector_norm(Yl - Y, dim=1) / torch.linalg.vector_norm(Y, dim=1)).max().item()
+    assert err <= 1e-12
+    if n <= 12:
+        op = O.PenalizedOperator(n, k, A, e, masks, "crossdof")
+        assert relerr_cols(Yl.cpu().numpy(), op.apply_fourier(X.cpu().numpy())) <= 1e-12
