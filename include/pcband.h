@@ -183,6 +183,7 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "fuse_resid"   1: residual + K_P^{-1} fused into the A-image block update; 0 (default): separate
  *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)
  *   "update_warps" 4 (default), 8 or 16 warps per block-update CTA (process-wide tuning knob)
+ *   "gram_ks"      2 (default) or 1 warp groups splitting each Gram row chunk (process-wide knob)
  */
 int pc_set_option(pc_ctx *ctx, const char *key, double value);
 

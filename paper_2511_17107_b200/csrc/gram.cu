@@ -9,24 +9,25 @@
 #include "kernels.h"
 #include "dmma.cuh"
 
-template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS = 1>
 struct GramCfg {
   static constexpr int BM = WARPS_M * WM * 8, BN = WARPS_N * WN * 8;
-  static constexpr int THREADS = 32 * WARPS_M * WARPS_N;
+  static constexpr int THREADS = 32 * WARPS_M * WARPS_N * KS;  // KS warp groups split each chunk's rows
   static constexpr int PITCH = 2 * KC + 8;  // doubles per column, 8 mod 16: 16-B fragment loads conflict-free
   static constexpr size_t SMEM = (size_t)STAGES * (BM + BN) * PITCH * sizeof(double);
 };
 
-template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
-__global__ void __launch_bounds__(GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>::THREADS)
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS>
+__global__ void __launch_bounds__(GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>::THREADS)
 gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_per_split, int nmb, cplx* partial) {
-  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
   constexpr int BM = Cfg::BM, BN = Cfg::BN, NTH = Cfg::THREADS, PITCH = Cfg::PITCH;
   extern __shared__ __align__(16) double gsm[];
   double* As = gsm;                           // [STAGES][BM][PITCH]
   double* Bs = gsm + STAGES * BM * PITCH;     // [STAGES][BN][PITCH]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int wm = warp % WARPS_M, wn = warp / WARPS_M;
+  const int kg = warp / (WARPS_M * WARPS_N);  // row group of this warp within a chunk
+  const int wm = warp % WARPS_M, wn = (warp / WARPS_M) % WARPS_N;
   const int mb = blockIdx.x % nmb, nb = blockIdx.x / nmb;
   const int m0 = mb * BM, n0 = nb * BN;
   const long long r0 = (long long)blockIdx.y * rows_per_split;
@@ -84,7 +85,7 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
       const double* A = As + st * BM * PITCH;
       const double* B = Bs + st * BN * PITCH;
 #pragma unroll 2
-      for (int s4 = 0; s4 < KC / 4; s4++) {
+      for (int s4 = kg; s4 < KC / 4; s4 += KS) {
         const int kk = 2 * (4 * s4 + (lane & 3));  // complex row 4 s4 + (lane & 3), interleaved doubles
         double ar[WM], ai[WM], ad[WM], br[WN], bi[WN], bs[WN];
 #pragma unroll
@@ -115,6 +116,47 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
   }
   cp_async_wait<0>();
 
+  if constexpr (KS > 1) {
+    // fold the row groups' accumulators into group 0 through shared memory (fixed order)
+    constexpr int NACC = WM * WN * 6;
+    double* red = gsm;  // pipeline buffers are free now
+    __syncthreads();
+    const int wl = warp % (WARPS_M * WARPS_N);
+    for (int g = 1; g < KS; g++) {
+      if (kg == g) {
+        double* dst = red + ((size_t)wl * 32 + lane) * NACC;
+        int t = 0;
+#pragma unroll
+        for (int mt = 0; mt < WM; mt++)
+#pragma unroll
+          for (int nt = 0; nt < WN; nt++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              dst[t++] = p1[mt][nt][e];
+              dst[t++] = p2[mt][nt][e];
+              dst[t++] = p3[mt][nt][e];
+            }
+      }
+      __syncthreads();
+      if (kg == 0) {
+        const double* src = red + ((size_t)wl * 32 + lane) * NACC;
+        int t = 0;
+#pragma unroll
+        for (int mt = 0; mt < WM; mt++)
+#pragma unroll
+          for (int nt = 0; nt < WN; nt++)
+#pragma unroll
+            for (int e = 0; e < 2; e++) {
+              p1[mt][nt][e] += src[t++];
+              p2[mt][nt][e] += src[t++];
+              p3[mt][nt][e] += src[t++];
+            }
+      }
+      __syncthreads();
+    }
+    if (kg != 0) return;
+  }
+
   cplx* out = partial + (size_t)blockIdx.y * p * q;
 #pragma unroll
   for (int mt = 0; mt < WM; mt++)
@@ -139,13 +181,17 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
   G[idx] = acc;
 }
 
+static int g_gram_ks = 2;  // pc_set_option "gram_ks" (1 or 2), process-wide tuning knob
+void set_gram_ks(int k) { g_gram_ks = (k == 1) ? 1 : 2; }
+
 size_t gram_partial_bytes(int p, int q) { return (size_t)4 * 148 * p * q * sizeof(cplx) + 4096; }
 
-template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES>
+template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS = 1>
 static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                      cudaStream_t st) {
-  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
-  auto kern = gram_kernel<WM, WN, WARPS_M, WARPS_N, KC, STAGES>;
+  using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
+  static_assert(KS == 1 || (size_t)WARPS_M * WARPS_N * 32 * WM * WN * 6 * 8 <= Cfg::SMEM, "reduction buffer");
+  auto kern = gram_kernel<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
   static int ctas_per_sm = 0;
   if (!ctas_per_sm) {
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
@@ -181,17 +227,26 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     const double cost = area * (1.0 + 0.04 * (nbm * nbn - 1));
     if (cost < best_cost - 1e-9) { best_cost = cost; best = i; }
   }
+  // KS = 2 (two warp groups per chunk, accumulators folded at the end) where the fold buffer fits
+#define PC_GRAM_CASE(WM_, WN_, WAM, WAN, KC_, ST_)                                          \
+  if (g_gram_ks == 2 && (size_t)WAM * WAN * 32 * WM_ * WN_ * 48 <=                          \
+                            GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM)                  \
+    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, (WAM * WAN * 32 * WM_ * WN_ * 48 <=               \
+                                            (int)GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM) ? 2 : 1>( \
+        S, p, T, q, len, G, partial, st);                                                   \
+  else                                                                                      \
+    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, 1>(S, p, T, q, len, G, partial, st);
   switch (best) {
-    case 0: run_gram<3, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 1: run_gram<3, 2, 2, 3, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 2: run_gram<2, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 3: run_gram<2, 2, 2, 2, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 4: run_gram<5, 1, 1, 5, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 5: run_gram<5, 1, 1, 8, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 6: run_gram<4, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 7: run_gram<5, 2, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    case 8: run_gram<5, 3, 2, 4, 16, 2>(S, p, T, q, len, G, partial, st); break;
-    case 9: run_gram<3, 1, 1, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
-    default: run_gram<3, 3, 2, 4, 16, 3>(S, p, T, q, len, G, partial, st); break;
+    case 0: PC_GRAM_CASE(3, 2, 2, 4, 16, 3) break;
+    case 1: PC_GRAM_CASE(3, 2, 2, 3, 16, 3) break;
+    case 2: PC_GRAM_CASE(2, 2, 2, 4, 16, 3) break;
+    case 3: PC_GRAM_CASE(2, 2, 2, 2, 16, 3) break;
+    case 4: PC_GRAM_CASE(5, 1, 1, 5, 16, 3) break;
+    case 5: PC_GRAM_CASE(5, 1, 1, 8, 16, 3) break;
+    case 6: PC_GRAM_CASE(4, 2, 2, 4, 16, 3) break;
+    case 7: PC_GRAM_CASE(5, 2, 2, 4, 16, 3) break;
+    case 8: PC_GRAM_CASE(5, 3, 2, 4, 16, 2) break;
+    case 9: PC_GRAM_CASE(3, 1, 1, 4, 16, 3) break;
+    default: PC_GRAM_CASE(3, 3, 2, 4, 16, 3) break;
   }
 }

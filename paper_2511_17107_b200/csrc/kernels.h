@@ -70,6 +70,7 @@ void launch_pw_scatter(const MutColPtrs& X, const PwEntry* e, int ne, int n3, cu
 // dense block algebra ------------------------------------------------------------------------
 // G (p x q, column-major, ld p) = S^H T over rows [0, len): S p columns, T q columns.
 size_t gram_partial_bytes(int p, int q);
+void set_gram_ks(int k);  // tuning knob: 1 or 2 warp groups per Gram chunk
 // [G_M | G_A] (p x 2p) from Gp = S^H [W P AW AP] (p x 2c), S = [X W P], b = |X|, c = |W| + |P|,
 // assuming X^H X = I, X^H A X = diag(lambda) (Ritz vectors of the previous Rayleigh-Ritz step).
 void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);

@@ -385,6 +385,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
+  else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
