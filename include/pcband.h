@@ -180,7 +180,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  wanted columns; -1: all b columns)
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
  *                  Diagonal/Trivial mode); 0: 7-pass pipeline with the standalone stencil
- *   "fuse_resid"   1: residual + K_P^{-1} fused into the A-image block update; 0 (default): separate
+ *   "fuse_resid"   1 (default): both block updates + next residual + K_P^{-1} in one pass; 0: two
+ *                  update launches and a separate residual pass
  *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)
  *   "update_warps" 4 (default), 8 or 16 warps per block-update CTA (process-wide tuning knob)
  *   "gram_ks"      2 (default) or 1 warp groups splitting each Gram row chunk (process-wide knob)

@@ -56,9 +56,12 @@ constexpr int pow2_div(int n, int cap) {
   while (t < cap && n % (2 * t) == 0) t *= 2;
   return t;
 }
+#ifndef PC_ZTP
+#define PC_ZTP 8
+#endif
 template <int N, int C>
 struct TileCfg {
-  static constexpr int TP = pow2_div(N, C == 3 ? 8 : 16);
+  static constexpr int TP = pow2_div(N, C == 3 ? PC_ZTP : 16);
   static constexpr int TPP = TP + 1;
   static constexpr int NT = TP * FftPlan<N>::R1;
   // x pass: [c][p][j] with pitch N+1 (tile rows contiguous as in HBM: conflict-free cp.async writes);

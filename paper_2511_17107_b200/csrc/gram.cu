@@ -229,9 +229,11 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
   }
   // KS = 2 (two warp groups per chunk, accumulators folded at the end) where the fold buffer fits
 #define PC_GRAM_CASE(WM_, WN_, WAM, WAN, KC_, ST_)                                          \
-  if (g_gram_ks == 2 && (size_t)WAM * WAN * 32 * WM_ * WN_ * 48 <=                          \
+  if (g_gram_ks == 2 && WM_ * WN_ <= 6 &&                                \
+      (size_t)WAM * WAN * 32 * WM_ * WN_ * 48 <=                                            \
                             GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM)                  \
-    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, (WAM * WAN * 32 * WM_ * WN_ * 48 <=               \
+    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, (WM_ * WN_ <= 6 &&             \
+                                            WAM * WAN * 32 * WM_ * WN_ * 48 <=               \
                                             (int)GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM) ? 2 : 1>( \
         S, p, T, q, len, G, partial, st);                                                   \
   else                                                                                      \

@@ -83,14 +83,15 @@ void set_update_warps(int w);  // tuning knob (4, 8 or 16 warps per update CTA)
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st);
 
-// A-image update fused with the next residual (update_resid.cu): Y1/Y2 as in launch_update (r <= 32),
-// then R = Y2 - Xn diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if
-// deflate0), per-CTA |R_c|^2, |Xn_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  Returns the grid
+// Both block updates fused with the next residual (update_all.cu): for S and AS as in launch_update
+// (Y1s/Y1a: P', AP' columns [split, p) only, null columns skipped; Y2s/Y2a: X', AX'), then
+// R = AX' - X' diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if deflate0),
+// per-CTA |R_c|^2, |X'_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  r <= 32.  Returns the grid
 // (<= max_grid) for launch_reduce_partial.
-int launch_update_resid(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
-                        const MutColPtrs& Y2, const ColPtrs& Xn, const MutColPtrs& W, const double* lam, int n,
-                        const cplx* kt, double gamma, double thr, int deflate0, double* partial, int max_grid,
-                        cudaStream_t st);
+int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
+                      const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
+                      const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
+                      int deflate0, double* partial, int max_grid, cudaStream_t st);
 
 // Rayleigh-Ritz ------------------------------------------------------------------------------
 // G = [G_M | G_A] (p x 2p, column-major ld p).  Outputs C (p x nb, ld p), lambda (nb), info[0] = rank,

@@ -92,7 +92,7 @@ struct pc_ctx {
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
-  int fuse_resid = 0;          // residual + K_P^{-1} fused into the A-image update (update_resid.cu)
+  int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
@@ -1013,40 +1013,38 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
                                                   std::to_string(rank) + " < " + std::to_string(b) + ")");
       haveP = false;  // restart without the P block
     }
-    // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images
+    // updates: P' = [W P] C_wp (phase 1), X' = S C (phase 2); same for A-images.  P' only for the
+    // columns that can receive W (the others never use P).
     {
-      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + (c->fuse_resid ? 84.0 * c->n3 * b : 0.0),
-              2 * 16.0 * len * (p + b + nw) + (c->fuse_resid ? 16.0 * len * (b + nw) : 0.0));
-      ColPtrs S;
-      MutColPtrs Y1, Y2;
+      ColPtrs S, AS;
+      MutColPtrs Y1, Y2, Y1a, Y2a;
       ccols(sX, all, S, 0);
       ccols(WW, act, S, b);
       if (haveP) ccols(sP, act, S, b + na);
+      ccols(sAX, all, AS, 0);
+      ccols(AWW, act, AS, b);
+      if (haveP) ccols(sAP, act, AS, b + na);
       mcols(sPn, all, Y1, 0);
       mcols(sXn, all, Y2, 0);
-      for (int j = nw; j < b; j++) Y1.p[j] = nullptr;  // columns that never get W never use P
-      launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
-      ccols(sAX, all, S, 0);
-      ccols(AWW, act, S, b);
-      if (haveP) ccols(sAP, act, S, b + na);
-      mcols(sAPn, all, Y1, 0);
-      mcols(sAXn, all, Y2, 0);
-      for (int j = nw; j < b; j++) Y1.p[j] = nullptr;
+      mcols(sAPn, all, Y1a, 0);
+      mcols(sAXn, all, Y2a, 0);
+      for (int j = nw; j < b; j++) Y1.p[j] = Y1a.p[j] = nullptr;
       if (c->fuse_resid) {
-        // A-image update + next residual R = AX' - X' Lambda', W = K_P^{-1} R (WW is free again: the
-        // S-update above consumed it), |R|^2 and |X'|^2 partials
-        ColPtrs Xn;
+        // both updates + the next residual R = AX' - X' Lambda', W = K_P^{-1} R (each row tile's W is
+        // read into shared memory by the S phase before the same CTA overwrites it), |R|^2, |X'|^2
+        Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + 84.0 * c->n3 * b,
+                16.0 * len * (2 * p + 2 * (b + nw) + nw));
         MutColPtrs W;
-        ccols(sXn, all, Xn, 0);
         mcols(WW, all, W, 0);
         for (int j = nw; j < b; j++) W.p[j] = nullptr;
-        const int g = launch_update_resid(S, p, dC, p, b, b, &Y1, Y2, Xn, W, dLam, c->n, c->d_ktab, c->cur_gamma,
-                                          c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+        const int g = launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                        c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
-        c->launches += 1;
         resid_ready = true;
       } else {
+        Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b, 2 * 16.0 * len * (p + b + nw));
         launch_update(S, p, dC, p, b, b, &Y1, Y2, nullptr, len, st);
+        launch_update(AS, p, dC, p, b, b, &Y1a, Y2a, nullptr, len, st);
       }
     }
     std::swap(sX, sXn);

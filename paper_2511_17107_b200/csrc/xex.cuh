@@ -9,66 +9,101 @@
 #pragma once
 #include "fft_pass.cuh"
 
-// Two-step Stockham FFT of npen length-N pencils held in shared memory at addr(pencil, j).
-// Step B runs in rounds of complete pencils so the in-place write never clobbers unread input.
-template <int N, int DIR, class Addr>
-DEV void smem_fft(cplx* s, const cplx* tw, int npen, Addr addr) {
-  constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
-  const int tid = threadIdx.x, nt = blockDim.x;
-  for (int it = tid; it < npen * R2; it += nt) {
-    const int pen = it % npen, j2 = it / npen;
-    cplx v[R1];
-#pragma unroll
-    for (int j1 = 0; j1 < R1; j1++) v[j1] = s[addr(pen, j2 + R2 * j1)];
-    Dft<R1, DIR>::run(v);
-#pragma unroll
-    for (int k1 = 0; k1 < R1; k1++) {
-      cplx w = tw[(j2 * k1) % N];
-      if (DIR > 0) w.y = -w.y;
-      s[addr(pen, j2 + R2 * k1)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
-    }
-  }
-  __syncthreads();
-  const int ppr = nt / R1 > 0 ? nt / R1 : 1;
-  for (int p0 = 0; p0 < npen; p0 += ppr) {
-    const int pen = p0 + tid % ppr, k1 = tid / ppr;
-    const bool act = (tid < ppr * R1) && pen < npen;
-    cplx v[R2];
-    if (act) {
-#pragma unroll
-      for (int j2 = 0; j2 < R2; j2++) v[j2] = s[addr(pen, R2 * k1 + j2)];
-      Dft<R2, DIR>::run(v);
-    }
-    __syncthreads();
-    if (act) {
-#pragma unroll
-      for (int k2 = 0; k2 < R2; k2++) s[addr(pen, k1 + R1 * k2)] = v[k2];
-    }
-    __syncthreads();
-  }
-}
+// Row pencils of length N = R1 * R2 (two-step Stockham).  Shared rows have pitch P (odd).  Two index
+// layouts inside a row: "natural" j (0..N-1) and "mid" j2 * S1 + k1 (after the first step: R2 DFTs of
+// size R1 over j = j2 + R2 j1, twiddled), S1 = R1 rounded up to odd, so that lanes with consecutive j2
+// (first step) and lanes with consecutive k1 (second step) both hit distinct banks.
+template <int N>
+struct XRow {
+  static constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
+  static constexpr int S1 = (R1 % 2 == 0) ? R1 + 1 : R1;
+  static constexpr int L = ((R2 - 1) * S1 + R1 > N) ? (R2 - 1) * S1 + R1 : N;
+  static constexpr int P = (L % 2 == 1) ? L : L + 1;
+};
 
 template <int N>
 struct XexCfg {
   static constexpr int TP = pow2_div(N, 8);   // output rows per tile
   static constexpr int RP = TP + 2;           // rows held (1 halo row each side)
-  static constexpr int NP1 = N + 1;           // row pitch in complex (odd: conflict-free fragments)
+  static constexpr int P = XRow<N>::P;        // row pitch in complex
   static constexpr int NT = 256;
   static constexpr int PPT = (N * TP + NT - 1) / NT;  // stencil points per thread
-  static constexpr size_t SMEM = (size_t)3 * RP * NP1 * sizeof(cplx) + (size_t)N * sizeof(cplx) + (size_t)RP * N;
+  static constexpr size_t SMEM = (size_t)3 * RP * P * sizeof(cplx) + (size_t)N * sizeof(cplx) + (size_t)RP * N;
 };
 
+// First Stockham step for npen rows: R2 DFTs of size R1 (input stride R2) + twiddles, result in the
+// mid layout of the row.  Input element j of pencil pen comes from load(pen, j) (global or shared).
+// Thread item = (pen, j2) with j2 fastest: R2 lanes read R2 consecutive inputs of one pencil.
+template <int N, int DIR, class Load, class Row>
+DEV void xrow_step1(cplx* s, const cplx* tw, int npen, Load load, Row row, bool sync_inplace) {
+  using X = XRow<N>;
+  constexpr int R1 = X::R1, R2 = X::R2, S1 = X::S1, P = X::P;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = nt / R2;  // pencils per round
+  for (int p0 = 0; p0 < npen; p0 += per) {
+    const int pen = p0 + tid / R2, j2 = tid % R2;
+    const bool act = (tid < per * R2) && pen < npen;
+    cplx v[R1];
+    if (act) {
+#pragma unroll
+      for (int j1 = 0; j1 < R1; j1++) v[j1] = load(pen, j2 + R2 * j1);
+      Dft<R1, DIR>::run(v);
+    }
+    if (sync_inplace) __syncthreads();
+    if (act) {
+      cplx* d = s + row(pen) * P + j2 * S1;
+#pragma unroll
+      for (int k1 = 0; k1 < R1; k1++) {
+        cplx w = tw[(j2 * k1) % N];
+        if (DIR > 0) w.y = -w.y;
+        d[k1] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+      }
+    }
+    if (sync_inplace) __syncthreads();
+  }
+}
+
+// Second step: R1 DFTs of size R2 from the mid layout; output k = k1 + R1 k2 goes to store(pen, k, v).
+// Thread item = (pen, k1) with k1 fastest.  sync_inplace: the store writes the same shared rows.
+template <int N, int DIR, class Store, class Row>
+DEV void xrow_step2(const cplx* s, int npen, Store store, Row row, bool sync_inplace) {
+  using X = XRow<N>;
+  constexpr int R1 = X::R1, R2 = X::R2, S1 = X::S1, P = X::P;
+  const int tid = threadIdx.x, nt = blockDim.x;
+  const int per = nt / R1;
+  for (int p0 = 0; p0 < npen; p0 += per) {
+    const int pen = p0 + tid / R1, k1 = tid % R1;
+    const bool act = (tid < per * R1) && pen < npen;
+    cplx v[R2];
+    if (act) {
+      const cplx* src = s + row(pen) * P + k1;
+#pragma unroll
+      for (int j2 = 0; j2 < R2; j2++) v[j2] = src[j2 * S1];
+      Dft<R2, DIR>::run(v);
+    }
+    if (sync_inplace) __syncthreads();
+    if (act) {
+#pragma unroll
+      for (int k2 = 0; k2 < R2; k2++) store(pen, k1 + R1 * k2, v[k2]);
+    }
+    if (sync_inplace) __syncthreads();
+  }
+}
+
 // MODE: 0 diagonal, 1 crossdof with only eps_12, 2 trivial
+#ifndef PC_XEX_MINB
+#define PC_XEX_MINB 2
+#endif
 template <int N, int MODE>
-__global__ void __launch_bounds__(XexCfg<N>::NT, 3)
+__global__ void __launch_bounds__(XexCfg<N>::NT, PC_XEX_MINB)
 xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
            double scale, int zoff) {
   using Cfg = XexCfg<N>;
-  constexpr int TP = Cfg::TP, RP = Cfg::RP, NP1 = Cfg::NP1, NT = Cfg::NT, PPT = Cfg::PPT;
+  constexpr int TP = Cfg::TP, RP = Cfg::RP, P = Cfg::P, NT = Cfg::NT, PPT = Cfg::PPT;
   constexpr int N3 = N * N * N;
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* s = reinterpret_cast<cplx*>(smem_raw);  // [c][row][j] = (c*RP + row)*NP1 + j (rows as in HBM)
-  cplx* tw = s + 3 * RP * NP1;
+  cplx* s = reinterpret_cast<cplx*>(smem_raw);  // row (c*RP + r) at s + row * P
+  cplx* tw = s + 3 * RP * P;
   uint8_t* mk8 = reinterpret_cast<uint8_t*>(tw + N);  // [row][x]
   const int tid = threadIdx.x;
   const int z = zoff + blockIdx.x / (N / TP), y0 = (blockIdx.x % (N / TP)) * TP;
@@ -76,30 +111,23 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   const cplx* gin = in.p[col];
   cplx* gout = out.p[col];
 
-  // Rows held per component (smem row r <-> y = y0 - 1 + r): S_12^T v1 needs E^1 at y0-1 (r = 0),
-  // S_12 v2 needs E^2 at y0+TP (r = TP+1); E^3 and the pointwise modes need only r = 1..TP.
-  // pencil list: component 0 rows [lo0, lo0+n0), component 1 rows [1, 1+n1), component 2 rows [1, 1+TP)
-  constexpr int n0 = (MODE == 1) ? TP + 1 : TP, lo0 = (MODE == 1) ? 0 : 1;
-  constexpr int n1 = (MODE == 1) ? TP + 1 : TP;
-  constexpr int NPEN = n0 + n1 + TP;
-  auto pen_row = [&](int pen, int& c, int& r) {
-    if (pen < n0) { c = 0; r = lo0 + pen; }
-    else if (pen < n0 + n1) { c = 1; r = 1 + pen - n0; }
-    else { c = 2; r = 1 + pen - n0 - n1; }
-  };
-  for (int e = tid; e < NPEN * N; e += NT) {
-    const int j = e % N;
-    int c, r;
-    pen_row(e / N, c, r);
+  // Rows held per component (smem row r <-> y = y0 - 1 + r, r = 0 .. TP+1).  Only S_12 needs the halo
+  // rows (E^1 at y0-1, E^2 at y0+TP); in MODE 1 all three components hold all RP rows so the pencil
+  // list is uniform (pencil = smem row c*RP + r).
+  constexpr int NPEN = (MODE == 1) ? 3 * RP : 3 * TP;
+  auto prow = [](int pen) { return (MODE == 1) ? pen : (pen / TP) * RP + 1 + pen % TP; };
+  auto grow = [&](int row) {  // global offset of smem row
+    const int c = row / RP, r = row % RP;
     const int y = (y0 - 1 + r + N) % N;
-    cp_async16(&s[(c * RP + r) * NP1 + j], gin + (long long)c * N3 + ((long long)z * N + y) * N + j);
-  }
+    return (long long)c * N3 + ((long long)z * N + y) * N;
+  };
   if constexpr (N % 16 == 0) {
     for (int e = tid; e < RP * (N / 16); e += NT) {
       const int j = (e % (N / 16)) * 16, r = e / (N / 16);
       const int y = (y0 - 1 + r + N) % N;
       cp_async16(&mk8[r * N + j], mask + ((long long)z * N + y) * N + j);
     }
+    cp_async_commit();
   } else {
     for (int e = tid; e < RP * N; e += NT) {
       const int j = e % N, r = e / N;
@@ -107,17 +135,15 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
       mk8[e] = __ldg(mask + ((long long)z * N + y) * N + j);
     }
   }
-  cp_async_commit();
   for (int j = tid; j < N; j += NT) tw[j] = ldg(twg + j);
-  cp_async_wait<0>();
   __syncthreads();
 
-  // inverse x-DFT of the held rows
-  smem_fft<N, +1>(s, tw, NPEN, [&](int pen, int j) {
-    int c, r;
-    pen_row(pen, c, r);
-    return (c * RP + r) * NP1 + j;
-  });
+  // inverse x-DFT of the held rows: first step straight from HBM (R2 lanes read R2 consecutive complex)
+  xrow_step1<N, +1>(s, tw, NPEN, [&](int pen, int j) { return ldg(gin + grow(prow(pen)) + j); }, prow, false);
+  __syncthreads();
+  xrow_step2<N, +1>(s, NPEN, [&](int pen, int k, cplx v) { s[prow(pen) * P + k] = v; }, prow, true);
+  if constexpr (N % 16 == 0) cp_async_wait<0>();
+  __syncthreads();
 
   // M_eps on the TP output rows (registers first: the stencil reads neighbours)
   cplx w[PPT][3];
@@ -128,7 +154,7 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
     const int x = e % N, r = 1 + e / N;
     const uint8_t mp = mk8[r * N + x];
     const double i1 = (mp & 1) ? 1.0 : 0.0, i2 = (mp & 2) ? 1.0 : 0.0, i3 = (mp & 4) ? 1.0 : 0.0;
-    const cplx v1 = s[(0 * RP + r) * NP1 + x], v2 = s[(1 * RP + r) * NP1 + x], v3 = s[(2 * RP + r) * NP1 + x];
+    const cplx v1 = s[(0 * RP + r) * P + x], v2 = s[(1 * RP + r) * P + x], v3 = s[(2 * RP + r) * P + x];
     cplx w1 = (1.0 + ec.d[0] * i1) * v1, w2 = (1.0 + ec.d[1] * i2) * v2, w3 = (1.0 + ec.d[2] * i3) * v3;
     if (MODE == 1) {
       const int xm = (x == 0) ? N - 1 : x - 1, xp = (x == N - 1) ? 0 : x + 1;
@@ -141,7 +167,7 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
         for (int bb = 0; bb < 2; bb++) {
           const int rr = r + bb, xx = qx[a];
           const double wgt = i1 + ((mk8[rr * N + xx] & 2) ? 1.0 : 0.0);
-          acc = acc + wgt * s[(1 * RP + rr) * NP1 + xx];
+          acc = acc + wgt * s[(1 * RP + rr) * P + xx];
         }
       w1 = w1 + 0.125 * cmul(ec.e[0], acc);
       // S_12^T v1 (into w2): q in {x, x+1} x {y-1, y}, weight I1(q) + I2(p)
@@ -153,7 +179,7 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
         for (int bb = 0; bb < 2; bb++) {
           const int rr = r - 1 + bb, xx = qx2[a];
           const double wgt = i2 + ((mk8[rr * N + xx] & 1) ? 1.0 : 0.0);
-          acc2 = acc2 + wgt * s[(0 * RP + rr) * NP1 + xx];
+          acc2 = acc2 + wgt * s[(0 * RP + rr) * P + xx];
         }
       w2 = w2 + 0.125 * cmul(conjg(ec.e[0]), acc2);
     } else if (MODE == 2) {
@@ -174,15 +200,15 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
     if (e >= N * TP) break;
     const int x = e % N, r = 1 + e / N;
 #pragma unroll
-    for (int c = 0; c < 3; c++) s[(c * RP + r) * NP1 + x] = w[t][c];
+    for (int c = 0; c < 3; c++) s[(c * RP + r) * P + x] = w[t][c];
   }
   __syncthreads();
 
-  // forward x-DFT of the TP output rows
-  smem_fft<N, -1>(s, tw, 3 * TP, [&](int pen, int j) { return ((pen / TP) * RP + 1 + pen % TP) * NP1 + j; });
-
-  for (int e = tid; e < 3 * TP * N; e += NT) {
-    const int j = e % N, r = (e / N) % TP, c = e / (N * TP);
-    gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + j] = s[(c * RP + 1 + r) * NP1 + j];
-  }
+  // forward x-DFT of the TP output rows; the last step writes HBM directly (R1 consecutive complex)
+  auto orow = [](int pen) { return (pen / TP) * RP + 1 + pen % TP; };
+  xrow_step1<N, -1>(s, tw, 3 * TP, [&](int pen, int j) { return s[orow(pen) * P + j]; }, orow, true);
+  xrow_step2<N, -1>(s, 3 * TP, [&](int pen, int k, cplx v) {
+    const int c = pen / TP, r = pen % TP;
+    gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + k] = v;
+  }, orow, false);
 }
