@@ -237,7 +237,13 @@ int pc_history(const pc_ctx *ctx, double *out, int cap, int *block);
 /* Supported grid sizes: writes up to cap values into sizes, returns how many exist. */
 int pc_supported_n(int *sizes, int cap);
 
+/* Free the context.  Its large device workspaces go to a process-wide per-device cache that later
+ * contexts reuse (so create/destroy per problem avoids re-allocating ~16 GB at n = 128). */
 void pc_destroy(pc_ctx *ctx);
+
+/* Return the cached device blocks of `device` (all devices if device < 0) to the CUDA driver.  Only
+ * blocks of destroyed contexts are cached; live contexts are unaffected.  Thread-safe. */
+void pc_trim(int device);
 const char *pc_last_error(void);
 
 #ifdef __cplusplus

@@ -60,6 +60,7 @@ def lib():
         "pc_debug_heevj": (i, [dp, i, dp, dp, ip]),
         "pc_history": (i, [vp, dp, i, ip]),
         "pc_destroy": (None, [vp]),
+        "pc_trim": (None, [i]),
         "pc_last_error": (ctypes.c_char_p, []),
     }
     for name, (res, args) in sig.items():
@@ -224,6 +225,11 @@ def pc_history(ctx: Ctx):
     out = np.zeros(max(1, rows * b.value))
     lib().pc_history(ctx.h, _dptr(out), rows, ctypes.byref(b))
     return out[: rows * b.value].reshape(rows, b.value)
+
+
+def pc_trim(device=-1):
+    """Return cached device blocks of destroyed contexts to the driver (all devices by default)."""
+    lib().pc_trim(int(device))
 
 
 def pc_debug_heevj(A):

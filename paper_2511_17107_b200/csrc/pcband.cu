@@ -8,6 +8,8 @@
 #include <cmath>
 #include <cstdio>
 #include <cstring>
+#include <map>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -40,29 +42,82 @@ extern "C" const char* pc_last_error(void) { return g_err.c_str(); }
 // ------------------------------------------------------------------------------------------
 // context
 // ------------------------------------------------------------------------------------------
+// Process-wide cache of large device blocks: a destroyed context's workspace is kept and handed to the
+// next context on the same device (pc_create/pc_destroy per problem then costs no cudaMalloc/cudaFree
+// of the ~16 GB LOBPCG workspace).  pc_trim() returns the cached blocks to the driver; an allocation
+// failure trims and retries once.
+static std::mutex g_cache_mu;
+static std::multimap<std::pair<int, size_t>, void*> g_cache;  // (device, bytes) -> block
+
+static void* cache_take(size_t want, size_t* got) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  auto it = g_cache.lower_bound({dev, want});
+  if (it == g_cache.end() || it->first.first != dev || it->first.second > want + want / 4) return nullptr;
+  void* p = it->second;
+  *got = it->first.second;
+  g_cache.erase(it);
+  return p;
+}
+static void cache_put(void* p, size_t bytes) {
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  g_cache.insert({{dev, bytes}, p});
+}
+static void cache_trim(int dev) {
+  std::lock_guard<std::mutex> lk(g_cache_mu);
+  int cur = 0;
+  cudaGetDevice(&cur);
+  for (auto it = g_cache.begin(); it != g_cache.end();) {
+    if (dev < 0 || it->first.first == dev) {
+      cudaSetDevice(it->first.first);
+      cudaFree(it->second);
+      it = g_cache.erase(it);
+    } else {
+      ++it;
+    }
+  }
+  cudaSetDevice(cur);
+}
+
 struct DevBuf {
   void* p = nullptr;
   size_t bytes = 0;
   int ensure(size_t b) {
     if (b <= bytes) return PC_OK;
-    if (p) cudaFree(p);
-    p = nullptr;
-    bytes = 0;
+    release();
+    size_t got = 0;
+    if ((p = cache_take(b, &got)) != nullptr) {
+      bytes = got;
+      return PC_OK;
+    }
     cudaError_t e = cudaMalloc(&p, b);
     if (e != cudaSuccess) {
       cudaGetLastError();
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cache_trim(dev);
+      e = cudaMalloc(&p, b);
+    }
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      p = nullptr;
       return set_err(PC_ENOMEM, std::string("cudaMalloc(") + std::to_string(b) + "): " + cudaGetErrorString(e));
     }
     bytes = b;
     return PC_OK;
   }
   void release() {
-    if (p) cudaFree(p);
+    if (p) cache_put(p, bytes);
     p = nullptr;
     bytes = 0;
   }
   template <class T> T* as() const { return reinterpret_cast<T*>(p); }
 };
+
+extern "C" void pc_trim(int device) { cache_trim(device); }
 
 // pinned host staging: [0, 2048) norms, [2048, 2056) info ints, [PIN_PWV..) top-k |kappa|^2,
 // [PIN_PWI..) top-k mode ints, [PIN_PWE..) plane-wave scatter entries
