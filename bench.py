@@ -213,6 +213,9 @@ def main():
     ap.add_argument("--warm-start", action="store_true",
                     help="path continuation: contiguous k stretches per context, each k started from the "
                          "previous k's Ritz block (SURVEY f2; not the paper's cold start, reported separately)")
+    ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
+                    help="gloo + ranks sharing GPUs (rank -> device rank %% count): a functional test of the "
+                         "multi-rank path on a smaller box; numbers from it are not scaling results")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -226,10 +229,16 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.dist_backend == "gloo":
+        local = local % torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
+    cdev = dev if args.dist_backend == "nccl" else torch.device("cpu")  # collective buffers
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group("gloo")
 
     def barrier():
         if world > 1:
@@ -292,7 +301,7 @@ def main():
                         stats[k_][f_] += v_[f_]
                 else:
                     stats[k_] += v_
-    t = torch.tensor([ms], dtype=torch.float64, device=dev)
+    t = torch.tensor([ms], dtype=torch.float64, device=cdev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     ms_max = float(t.item())
@@ -303,8 +312,8 @@ def main():
     # the one collective of the method: all-gather of eigenvalues
     gathered = None
     if world > 1:
-        loc = torch.from_numpy(np.concatenate([np.array(idx)[:, None], om], axis=1)).to(dev)
-        out = torch.empty((world * loc.shape[0], loc.shape[1]), dtype=loc.dtype, device=dev)
+        loc = torch.from_numpy(np.concatenate([np.array(idx)[:, None], om], axis=1)).to(cdev)
+        out = torch.empty((world * loc.shape[0], loc.shape[1]), dtype=loc.dtype, device=cdev)
         dist.all_gather_into_tensor(out, loc)
         gathered = out.shape[0]
 
@@ -432,7 +441,7 @@ def main():
             c2.close()
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
-        tt = torch.tensor([te], dtype=torch.float64, device=dev)
+        tt = torch.tensor([te], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
         b = W.nev + 5
