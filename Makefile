@@ -2,7 +2,7 @@
 NVCC      ?= nvcc
 ARCH      := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS   := -std=c++17 --expt-relaxed-constexpr -O3 -lineinfo $(ARCH) -Xcompiler -fPIC -Xcompiler -Wall \
-             -Xptxas -warn-spills
+             -Xptxas -warn-spills $(EXTRA)
 SRC       := paper_2511_17107_b200/csrc
 BUILD     := build
 LIB       := paper_2511_17107_b200/libpcband.so

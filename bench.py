@@ -342,7 +342,7 @@ def main():
     alg_gbs = 336.0 * pts / (apply_ms * 1e6)
     # design traffic of the 5-pass fused pipeline used for this medium (eps_13 = eps_23 = 0): z+K_A^H,
     # y, x-DFT+M_eps+x-DFT (+1 B mask), y, z+K_A+gamma K_B (re-reads x^) = 4 x 96 + 144 + 1 B/pt
-    design_b = 529.0
+    design_b = 513.0  # 5 passes: 96+16, 96, 97, 96, 96+16 B per point per column
     design_gbs = design_b * pts / (apply_ms * 1e6)
     apply = {"cols": ncol, "ms": apply_ms, "alg_bytes_per_point_col": 336,
              "alg_gbs": alg_gbs, "frac_of_8tbs": alg_gbs / 8000.0, "frac_of_measured_hbm": alg_gbs / hbm,

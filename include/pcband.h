@@ -220,8 +220,10 @@ int pc_debug_heevj(const double *A_host, int n, double *w_host, double *V_host, 
 /*
  * pc_debug_pass — test entry: one pencil pass of the pc_apply pipeline on ncols columns (device,
  * ld).  kind 0: plain unnormalised 1-D DFT along axis (0 x, 1 y, 2 z), sign dir (-1: e^{-},
- * +1: e^{+}), output scaled by scale; kind 1: u = scale * K_A^H X then e^{+} DFT along z;
- * kind 2: e^{-} DFT along z of X then K_A (.) + gamma K_B XH.  Synchronous.
+ * +1: e^{+}), output scaled by scale; kind 1: u = scale * K_A^H X then e^{+} DFT along z, and
+ * g = gamma (kappa . X) written to XH (N^3 complex per column, same ld); kind 2: e^{-} DFT s along
+ * z of X then K_A s + conj(kappa) g with g read from XH (= gamma K_B xhat when XH holds the g of
+ * kind 1 applied to xhat).  Synchronous.
  */
 int pc_debug_pass(pc_ctx *ctx, const double k[3], int kind, int axis, int dir, const void *X, void *Y,
                   const void *XH, int ncols, long long ld, double scale);

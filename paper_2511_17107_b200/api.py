@@ -13,7 +13,7 @@ import os
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libpcband.so")
+LIB_PATH = os.environ.get("PCBAND_LIB") or os.path.join(_HERE, "libpcband.so")  # override: tuning builds
 
 PC_OK, PC_ENOTCONV = 0, 1
 PC_EINVAL, PC_ENOTPD, PC_ECUDA, PC_ENOMEM, PC_ENUMERIC = -1, -2, -3, -4, -5
@@ -58,6 +58,7 @@ def lib():
         "pc_stats": (i, [vp, dp, i]),
         "pc_supported_n": (i, [ip, i]),
         "pc_debug_heevj": (i, [dp, i, dp, dp, ip]),
+        "pc_debug_pass": (i, [vp, dp, i, i, i, vp, vp, vp, i, ll, d]),
         "pc_history": (i, [vp, dp, i, ip]),
         "pc_destroy": (None, [vp]),
         "pc_trim": (None, [i]),
@@ -230,6 +231,17 @@ def pc_history(ctx: Ctx):
 def pc_trim(device=-1):
     """Return cached device blocks of destroyed contexts to the driver (all devices by default)."""
     lib().pc_trim(int(device))
+
+
+def pc_debug_pass(ctx: Ctx, k, kind, axis, direction, X, Y, XH=None, scale=1.0):
+    """One FFT pass (test/tuning entry): kind 0 plain, 1 K_A^H-fused inverse z, 2 K_A + gamma K_B forward z
+    (XH = the apply input x_hat).  Runs on the legacy default stream and synchronises."""
+    kk = np.ascontiguousarray(np.asarray(k, dtype=np.float64).reshape(3))
+    px, nc, ld = _block(X)
+    py, _, _ = _block(Y)
+    pxh = _block(XH)[0] if XH is not None else None
+    _check(lib().pc_debug_pass(ctx.h, _dptr(kk), int(kind), int(axis), int(direction), px, py, pxh, nc, ld,
+                               float(scale)))
 
 
 def pc_debug_heevj(A):

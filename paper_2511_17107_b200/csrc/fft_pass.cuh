@@ -11,7 +11,10 @@
 // cp.async tile writes are contiguous like the HBM rows; odd pitches keep the FFT steps conflict-free.
 //
 // OP_KAH   (prologue): u = scale * (xhat x conj(kappa))   = K_A^H xhat
-// OP_KAG   (epilogue): y = kappa x s + gamma conj(kappa) (kappa . xhat)
+//          and the scalar g = gamma (kappa . xhat) of the penalty term to xh.p[col] (N^3 per column)
+// OP_KAG   (epilogue): y = kappa x s + conj(kappa) g  = K_A s + gamma K_B xhat
+//          with g read back from xh.p[col] (one complex per mode instead of re-reading the 3 components
+//          of xhat: 32 B per point per column of HBM traffic instead of 48)
 // with kappa_i(m) = sum_a ktab[(3 i + a) N + m_a]  (Dhat_i symbols, reading R3).
 #pragma once
 #include "kernels.h"
@@ -62,26 +65,27 @@ constexpr int pow2_div(int n, int cap) {
 template <int N, int C>
 struct TileCfg {
   static constexpr int TP = pow2_div(N, C == 3 ? PC_ZTP : 16);
-  static constexpr int TPP = TP + 1;
+  // C = 3 (the symbol-fused z passes): rows of TP >= 8 complex are whole 128-B bank sweeps, so the
+  // [c][j][p] layout needs no padding; the space goes to the z-pieces of the symbol table
+  static constexpr int TPP = (C == 3 && TP >= 8) ? TP : TP + 1;
   static constexpr int NT = TP * FftPlan<N>::R1;
   // x pass: [c][p][j] with pitch N+1 (tile rows contiguous as in HBM: conflict-free cp.async writes);
   // y/z passes: [c][j][p] with pitch TP+1.  Both odd pitches: conflict-free 16-B fragment accesses.
   static constexpr int SPAN = (TP * (N + 1) > N * TPP) ? TP * (N + 1) : N * TPP;
   // C = 1: persistent CTAs with a 2-stage prefetch pipeline; C = 3 (fused symbol passes, 3x the tile):
   // one tile per CTA and higher occupancy instead
-  static constexpr int STAGES = (C == 1) ? 2 : 1;
-  static constexpr size_t SMEM = (size_t)STAGES * C * SPAN * sizeof(cplx) + (size_t)N * sizeof(cplx);
+#ifndef PC_C3_STAGES
+#define PC_C3_STAGES 1
+#endif
+  static constexpr int STAGES = (C == 1) ? 2 : PC_C3_STAGES;
+  static constexpr int KTZ = (C == 3) ? 3 * N : 0;  // ktab z-pieces [3 comps][N]
+  static constexpr size_t SMEM = (size_t)STAGES * C * SPAN * sizeof(cplx) + (size_t)(N + KTZ) * sizeof(cplx);
 };
 
 // PassArgs: tw[j] = exp(-2 pi i j/N); ktab = [3 comps][3 axes][N] symbol pieces (OP_KAH/OP_KAG);
 // gamma (OP_KAG); scale (OP_KAH: folded 1/N^3; OP_NONE: applied at store if != 1).
 typedef PassArgsH PassArgs;
 
-template <int N>
-DEV cplx kappa_i(const cplx* kt, int i, int m1, int m2, int m3) {
-  const cplx* b = kt + 3 * i * N;
-  return ldg(b + m1) + ldg(b + N + m2) + ldg(b + 2 * N + m3);
-}
 
 // Tile geometry: element (c, j, p) of tile t -> offset within one column, and its mode triple.
 template <int N, int AXIS, int TP>
@@ -123,7 +127,8 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
   const int TPV = (N / TP) * ((AXIS != 2 && a.nz > 0) ? a.nz : N);  // tiles per component volume (z-range)
   extern __shared__ __align__(16) unsigned char smem_raw[];
   cplx* tw = reinterpret_cast<cplx*>(smem_raw);
-  cplx* stage_base = tw + N;  // [STAGES][C * SPAN]
+  cplx* ktz = tw + N;                             // [3][N]: ktab[(3 i + 2) N + m3] (C = 3 only)
+  cplx* stage_base = ktz + TileCfg<N, C>::KTZ;    // [STAGES][C * SPAN]
   constexpr int ST = TileCfg<N, C>::STAGES;
   auto SI = [](int c, int j, int p) { return AXIS == 0 ? (c * TP + p) * (N + 1) + j : (c * N + j) * TPP + p; };
   const int tid = threadIdx.x;
@@ -142,6 +147,9 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
   };
 
   for (int j = tid; j < N; j += NT) tw[j] = ldg(a.tw + j);
+  if constexpr (C == 3) {
+    for (int e = tid; e < 3 * N; e += NT) cp_async16(&ktz[e], a.ktab + (3 * (e / N) + 2) * N + e % N);
+  }
   int t = blockIdx.x;
   if (t < ntiles) load_tile(t, stage_base);
   cp_async_commit();
@@ -149,28 +157,44 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
     cplx* s = stage_base + (it % ST) * C * SPAN;
     if (ST > 1 && t + (int)gridDim.x < ntiles) load_tile(t + gridDim.x, stage_base + ((it + 1) % ST) * C * SPAN);
     cp_async_commit();
+    const TileMap<N, AXIS, TP> tm(t % TPV, a.z0);
+    // symbol passes: the (x, y) pieces of kappa are per-thread constants (see the prologue); their loads
+    // are issued before the tile wait so the latency overlaps it
+    cplx kxy[3];
+    if constexpr (C == 3) {
+      int m1, m2, m3;
+      tm.modes(0, tid % TP, m1, m2, m3);
+#pragma unroll
+      for (int i = 0; i < 3; i++) kxy[i] = ldg(a.ktab + 3 * i * N + m1) + ldg(a.ktab + (3 * i + 1) * N + m2);
+    }
     cp_async_wait<1>();
     __syncthreads();
 
-    const TileMap<N, AXIS, TP> tm(t % TPV, a.z0);
     const int cc = t / TPV;
     const int col = (C == 3) ? cc : cc / 3, comp0 = (C == 3) ? 0 : cc % 3;
     cplx* gout = out.p[col] + (long long)comp0 * N3;
 
     // ---- prologue: u = scale * (xhat x conj(kappa))
+    // Symbol-fused passes run along z (AXIS 2): a thread's elements share x = fixed_b + (tid % TP) and
+    // y = fixed_a, so kappa_i = [ktab_i,x(m1) + ktab_i,y(m2)] (per-thread constant) + ktab_i,z(m3); the
+    // EPT z-pieces are loaded together (unrolled) so their latencies overlap.
+    static_assert(OP == OP_NONE || (AXIS == 2 && NT % TP == 0 && (N * TP) % NT == 0), "symbol pass layout");
+    constexpr int EPT = (N * TP) / NT;
     if constexpr (OP == OP_KAH) {
-      for (int e = tid; e < N * TP; e += NT) {
-        int p = e % TP, j = e / TP;
-        int m1, m2, m3;
-        tm.modes(j, p, m1, m2, m3);
-        cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
-        cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
-        cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
+      const int p = tid % TP;
+      cplx* gkx = const_cast<cplx*>(xh.p[col]);
+#pragma unroll
+      for (int q = 0; q < EPT; q++) {
+        const int j = tid / TP + q * (NT / TP);
+        const cplx k1 = kxy[0] + ktz[j], k2 = kxy[1] + ktz[N + j], k3 = kxy[2] + ktz[2 * N + j];
         cplx x1 = s[SI(0, j, p)], x2 = s[SI(1, j, p)], x3 = s[SI(2, j, p)];
         // (x x conj k)_1 = x2 ck3 - x3 ck2, _2 = x3 ck1 - x1 ck3, _3 = x1 ck2 - x2 ck1
         cplx u1 = cmul(x2, conjg(k3)) - cmul(x3, conjg(k2));
         cplx u2 = cmul(x3, conjg(k1)) - cmul(x1, conjg(k3));
         cplx u3 = cmul(x1, conjg(k2)) - cmul(x2, conjg(k1));
+        // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T), kept for the last pass
+        const cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
+        gkx[tm.off(j, p)] = a.gamma * kx;
         s[SI(0, j, p)] = a.scale * u1;
         s[SI(1, j, p)] = a.scale * u2;
         s[SI(2, j, p)] = a.scale * u3;
@@ -212,24 +236,22 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
 
     // ---- store (with fused epilogue)
     if constexpr (OP == OP_KAG) {
-      const cplx* gx = xh.p[col];
-      for (int e = tid; e < N * TP; e += NT) {
-        int j, p;
-        if (AXIS == 0) { j = e % N; p = e / N; } else { p = e % TP; j = e / TP; }
-        int m1, m2, m3;
-        tm.modes(j, p, m1, m2, m3);
-        cplx k1 = kappa_i<N>(a.ktab, 0, m1, m2, m3);
-        cplx k2 = kappa_i<N>(a.ktab, 1, m1, m2, m3);
-        cplx k3 = kappa_i<N>(a.ktab, 2, m1, m2, m3);
-        int o = tm.off(j, p);
-        cplx x1 = ldg(gx + o), x2 = ldg(gx + N3 + o), x3 = ldg(gx + 2 * N3 + o);
-        cplx s1 = s[SI(0, j, p)], s2 = s[SI(1, j, p)], s3 = s[SI(2, j, p)];
-        // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T)
-        cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
-        kx = a.gamma * kx;
-        cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), kx);
-        cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), kx);
-        cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), kx);
+      // same element ownership as the prologue; x_hat (the apply input) and the z-pieces of kappa are
+      // loaded for all EPT elements first so the global latencies overlap
+      const cplx* gkx = xh.p[col];
+      const int p = tid % TP;
+      cplx g[EPT];
+#pragma unroll
+      for (int q = 0; q < EPT; q++) g[q] = ldg(gkx + tm.off(tid / TP + q * (NT / TP), p));
+#pragma unroll
+      for (int q = 0; q < EPT; q++) {
+        const int j = tid / TP + q * (NT / TP);
+        const int o = tm.off(j, p);
+        const cplx k1 = kxy[0] + ktz[j], k2 = kxy[1] + ktz[N + j], k3 = kxy[2] + ktz[2 * N + j];
+        const cplx s1 = s[SI(0, j, p)], s2 = s[SI(1, j, p)], s3 = s[SI(2, j, p)];
+        cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), g[q]);
+        cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), g[q]);
+        cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), g[q]);
         gout[o] = y1;
         gout[N3 + o] = y2;
         gout[2 * N3 + o] = y3;

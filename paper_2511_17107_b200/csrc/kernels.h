@@ -88,6 +88,7 @@ void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int s
 // R = AX' - X' diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if deflate0),
 // per-CTA |R_c|^2, |X'_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  r <= 32.  Returns the grid
 // (<= max_grid) for launch_reduce_partial.
+void set_update_tma(int v);  // tuning knob: 1 = bulk-copy (TMA) row tiles, 0 = per-thread cp.async
 int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                       const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,

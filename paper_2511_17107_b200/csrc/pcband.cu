@@ -137,6 +137,7 @@ struct pc_ctx {
   double cur_k[3] = {NAN, NAN, NAN};
   double cur_gamma = 0.0, cur_thr = 0.0;
   DevBuf ws;          // apply workspace
+  DevBuf kxws;        // apply workspace: gamma (kappa . xhat), N^3 per column (first pass -> last pass)
   int apply_chunk = 0;
   int guard = 5;
   double drop_tol = 1e-12;
@@ -392,6 +393,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   if (c->d_tw) cudaFree(c->d_tw);
   if (c->d_ktab) cudaFree(c->d_ktab);
   c->ws.release();
+  c->kxws.release();
   c->lob.release();
   c->small.release();
   c->gpart.release();
@@ -441,6 +443,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
+  else if (k == "update_tma") set_update_tma((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
@@ -534,9 +537,17 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   // column; the last pass also reads x_hat: 144 B), 5 log2(N) flops per point per component
   const double pts = (double)c->n3 * nc;
   const double fl = 15.0 * std::log2((double)n) * pts;
+  // gamma (kappa . xhat) per mode and column: written by the first pass, read by the last
+  const size_t kxb = (size_t)nc * c->n3 * sizeof(cplx);
+  if (kxb > c->kxws.bytes) {
+    cudaStreamSynchronize(st);
+    CHK(c->kxws.ensure(kxb));
+  }
+  ColPtrs KX;
+  for (int j = 0; j < nc; j++) KX.p[j] = c->kxws.as<cplx>() + (size_t)j * c->n3;
   {
-    Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 30.0 * pts, 96.0 * pts);
-    CHK(fft_pass(c, 2, +1, 1, X, Y, none, nc, inv_n3, st));
+    Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 38.0 * pts, 112.0 * pts);
+    CHK(fft_pass(c, 2, +1, 1, X, Y, KX, nc, inv_n3, st));
   }
   // z-plane-local media (eps_13 = eps_23 = 0 in CrossDoF; any Diagonal/Trivial medium): the x-passes
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
@@ -586,8 +597,8 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
       }
     }
     {
-      Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 40.0 * pts, 144.0 * pts);
-      CHK(fft_pass(c, 2, -1, 2, Wc, Y, X, nc, 1.0, st));
+      Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
+      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st));
     }
     return PC_OK;
   }
@@ -606,8 +617,8 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
     CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
   }
   {
-    Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 40.0 * pts, 144.0 * pts);
-    CHK(fft_pass(c, 2, -1, 2, Wc, Y, X, nc, 1.0, st));
+    Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
+    CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st));
   }
   return PC_OK;
 }

@@ -13,6 +13,7 @@
 #include "kernels.h"
 #include "dmma.cuh"
 #include "kp.cuh"
+#include "tma.cuh"
 
 constexpr int UA_SEG = 16;               // modes per tile
 constexpr int UA_ROWS = 3 * UA_SEG;      // rows per tile (3 components)
@@ -25,7 +26,9 @@ HD int ua_pitch4mod8(int p) {
   return x;
 }
 
-template <int NT>
+// TMA = true: the row tiles arrive by bulk copies (one 256-B run per column and component, issued by
+// warp 0, completion counted on one mbarrier per buffer) instead of per-thread 16-B cp.async.
+template <int NT, bool TMA>
 __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
     ColPtrs S, ColPtrs AS, int p, const cplx* __restrict__ C, int ldc, int r, int split, MutColPtrs Y1s,
     MutColPtrs Y2s, MutColPtrs Y1a, MutColPtrs Y2a, MutColPtrs Wout, const double* __restrict__ lam, int n,
@@ -33,6 +36,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   constexpr int NTW = (NT + 1) / 2;
   extern __shared__ __align__(16) double uasm[];
   __shared__ double red[4][NTW][4][2][2];
+  __shared__ __align__(8) unsigned long long mbar[2];
   const int n3 = n * n * n;
   const int pe = (p + 3) & ~3;
   const int PS = ua_pitch4mod8(pe);
@@ -47,9 +51,37 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   }
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
   const cplx* dummy = S.p[0];
+  unsigned phase[2] = {0u, 0u};
+  if constexpr (TMA) {
+    // padding columns [p, pe) are never written by the bulk copies: zero them once (0 * NaN = NaN)
+    for (int e = tid; e < 2 * (pe - p) * UA_RP; e += UA_THREADS) {
+      const int b = e / ((pe - p) * UA_RP), rem = e % ((pe - p) * UA_RP);
+      Buf[b * pe * UA_RP + p * UA_RP + rem] = mk(0, 0);
+    }
+    if (tid == 0) {
+      mbar_init(&mbar[0], 1);
+      mbar_init(&mbar[1], 1);
+    }
+    fence_proxy_async();
+    __syncthreads();
+  }
   auto load_tile = [&](int buf, const ColPtrs& src, long long t) {
     const long long m0 = t * UA_SEG;
     cplx* dst = Buf + buf * pe * UA_RP;
+    if constexpr (TMA) {
+      if (warp == 0) {
+        const int nv = (int)min((long long)UA_SEG, (long long)n3 - m0);
+        const unsigned bytes = (unsigned)nv * 16u;
+        fence_proxy_async();
+        if (lane == 0) mbar_arrive_expect_tx(&mbar[buf], bytes * 3u * (unsigned)p);
+        __syncwarp();
+        for (int e = lane; e < 3 * p; e += 32) {
+          const int m = e / 3, seg = e % 3;
+          tma_load_1d(dst + m * UA_RP + seg * UA_SEG, src.p[m] + (long long)seg * n3 + m0, bytes, &mbar[buf]);
+        }
+      }
+      return;
+    }
     for (int e = tid; e < UA_ROWS * pe; e += UA_THREADS) {
       const int m = e / UA_ROWS, rho = e % UA_ROWS;
       const int seg = rho / UA_SEG, rr = rho % UA_SEG;
@@ -132,8 +164,13 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
       }
     };
     // ---- S phase (buffer 0)
-    cp_async_wait<1>();  // the S tile of t has landed (the AS tile may still stream)
-    __syncthreads();
+    if constexpr (TMA) {
+      mbar_wait(&mbar[0], phase[0]);
+      phase[0] ^= 1u;
+    } else {
+      cp_async_wait<1>();  // the S tile of t has landed (the AS tile may still stream)
+      __syncthreads();
+    }
     zero();
     kloop(Buf, split, p);
     store(Y1s, false);
@@ -142,9 +179,14 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
     __syncthreads();  // buffer 0 is free
     if (more) load_tile(0, S, t + gridDim.x);
     // ---- AS phase (buffer 1)
-    if (more) cp_async_wait<1>();
-    else cp_async_wait<0>();
-    __syncthreads();
+    if constexpr (TMA) {
+      mbar_wait(&mbar[1], phase[1]);
+      phase[1] ^= 1u;
+    } else {
+      if (more) cp_async_wait<1>();
+      else cp_async_wait<0>();
+      __syncthreads();
+    }
     zero();
     const cplx* Ac = Buf + pe * UA_RP;
     kloop(Ac, split, p);
@@ -188,7 +230,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
     __syncthreads();  // buffer 1 is free
     if (more) load_tile(1, AS, t + gridDim.x);
   }
-  cp_async_wait<0>();
+  if constexpr (!TMA) cp_async_wait<0>();
 
   // deterministic reduction: lanes sharing (lane & 3) hold the same column -> xor over lane >> 2 bits
 #pragma unroll
@@ -220,7 +262,10 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   }
 }
 
-template <int NT>
+static int g_update_tma = 1;  // pc_set_option "update_tma" (process-wide tuning knob)
+void set_update_tma(int v) { g_update_tma = v ? 1 : 0; }
+
+template <int NT, bool TMA>
 static int run_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                           const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a,
                           const MutColPtrs& Y2a, const MutColPtrs& W, const double* lam, int n, const cplx* kt,
@@ -229,14 +274,14 @@ static int run_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx
   const size_t smem = (size_t)(2 * pe * UA_RP + NT * 8 * ps) * sizeof(cplx);
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(update_all_kernel<NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(update_all_kernel<NT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
   const long long n3 = (long long)n * n * n;
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
   const int occ = std::max(1, std::min(8, (int)((227 * 1024) / (smem + 2048))));
   const int grid = (int)std::min<long long>(std::min<long long>(ntiles, 148LL * occ), max_grid);
-  update_all_kernel<NT><<<grid, UA_THREADS, smem, st>>>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n,
+  update_all_kernel<NT, TMA><<<grid, UA_THREADS, smem, st>>>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n,
                                                          kt, gamma, thr, deflate0, partial);
   return grid;
 }
@@ -246,7 +291,9 @@ int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
                       int deflate0, double* partial, int max_grid, cudaStream_t st) {
 #define PC_UA(NT_)                                                                                                \
-  return run_update_all<NT_>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr, deflate0, \
+  return g_update_tma ? run_update_all<NT_, true>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt,     \
+                                                  gamma, thr, deflate0, partial, max_grid, st)                     \
+                      : run_update_all<NT_, false>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr, deflate0, \
                              partial, max_grid, st)
   if (r <= 8) PC_UA(1);
   if (r <= 16) PC_UA(2);

@@ -31,6 +31,6 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 st = api.pc_stats(ctx)
 pts = W.n ** 3 * ncol
-out = {"ms": ms, "alg_gbs": 336 * pts / ms / 1e6, "design_gbs": 529 * pts / ms / 1e6,
+out = {"ms": ms, "alg_gbs": 336 * pts / ms / 1e6, "design_gbs": 513 * pts / ms / 1e6,
        "classes": {k_: round(v["ms"] / reps, 4) for k_, v in st.items() if isinstance(v, dict) and v["count"]}}
 print(json.dumps(out))
