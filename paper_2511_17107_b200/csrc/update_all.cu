@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   }
 }
 
-static int g_update_tma = 1;  // pc_set_option "update_tma" (process-wide tuning knob)
+static int g_update_tma = 0;  // pc_set_option "update_tma": 1 = bulk copies (measured slower: 256-B runs)
 void set_update_tma(int v) { g_update_tma = v ? 1 : 0; }
 
 template <int NT, bool TMA>
