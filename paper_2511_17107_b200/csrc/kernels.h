@@ -94,6 +94,24 @@ int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
                       int deflate0, double* partial, int max_grid, cudaStream_t st);
 
+// Update + residual + K_P^{-1} + the next iteration's Gram blocks in one pass (update_gram.cu):
+// S = [X W P] (p columns, X first: split = b), outputs X', AX' (b columns), P', AP', W' (nw columns,
+// null pointers skipped), norm partials as launch_update_all, and the reduced Gram tiles in gred
+// (G1 = [X' W' P']^H [W' P' AP'], G2 = (AX')^H W' in 8x8 tiles).  Requires update_gram_supported().
+// Returns the grid (for launch_reduce_partial).
+bool update_gram_supported(int p, int b, int nw);
+struct UgFlops { double flops_per_row; };  // algorithmic Gram flops of the fused pass per row (8 per complex MAC)
+inline UgFlops ug_flops(int b, int nw) { return {8.0 * ((double)(b + 2 * nw) * 3 * nw + (double)b * nw)}; }
+size_t update_gram_partial_bytes(int b, int nw);
+int launch_update_gram(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int b, int nw,
+                       const MutColPtrs& Xo, const MutColPtrs& Po, const MutColPtrs& AXo, const MutColPtrs& APo,
+                       const MutColPtrs& Wo, const double* lam, int n, const cplx* kt, double gamma, double thr,
+                       int deflate0, double* npart, cplx* gpart, cplx* gred, int max_grid, cudaStream_t st);
+// [G_M | G_A] (p x 2p) of S = [X W_a P_a] from gred, Gww = W_a^H A W_a (na x na), lambda; act (device,
+// na ints) = the active columns among the nw W'/P' columns.
+void launch_ug_assemble(const cplx* red, int b, int nw, const int* act, int na, int haveP, const cplx* Gww,
+                        const double* lam, int p, cplx* G, cudaStream_t st);
+
 // Rayleigh-Ritz ------------------------------------------------------------------------------
 // G = [G_M | G_A] (p x 2p, column-major ld p).  Outputs C (p x nb, ld p), lambda (nb), info[0] = rank,
 // info[1] = sweeps of the last Jacobi.  Uses scratch (>= 4 p^2 complex).

@@ -149,6 +149,7 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
+  int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
@@ -158,7 +159,7 @@ struct pc_ctx {
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
-  DevBuf lob, small, gpart;
+  DevBuf lob, small, gpart, ugbuf;
   double* h_pinned = nullptr;
   cudaStream_t stream = nullptr;
   // profiling
@@ -394,6 +395,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   if (c->d_ktab) cudaFree(c->d_ktab);
   c->ws.release();
   c->kxws.release();
+  c->ugbuf.release();
   c->lob.release();
   c->small.release();
   c->gpart.release();
@@ -441,6 +443,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
+  else if (k == "fuse_gram") c->fuse_gram = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "update_tma") set_update_tma((int)v);
@@ -908,6 +911,21 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   size_t small_bytes = (2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) + 64;
   CHK(c->small.ensure(small_bytes));
   CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
+  // fused update + next-iteration Gram (update_gram.cu): only the first nw columns ever get W and P
+  const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
+  const bool ug_ok = c->fuse_gram && c->fuse_resid && update_gram_supported(maxp, b, nw);
+  cplx *dUgPart = nullptr, *dUgRed = nullptr, *dGww = nullptr;
+  int* dAct = nullptr;
+  int* hAct = reinterpret_cast<int*>(c->h_pinned + 3072);
+  if (ug_ok) {
+    const size_t pb = update_gram_partial_bytes(b, nw);
+    CHK(c->ugbuf.ensure(pb + (size_t)(48 * 64 + b * b) * sizeof(cplx) + 64 * sizeof(int)));
+    dUgPart = c->ugbuf.as<cplx>();
+    dUgRed = dUgPart + pb / sizeof(cplx);
+    dGww = dUgRed + 48 * 64;
+    dAct = reinterpret_cast<int*>(dGww + b * b);
+  }
+  bool fused_ready = false;  // dUgRed holds the Gram blocks of the current [X W P] (all nw W, P columns)
   cplx* dG = c->small.as<cplx>();
   cplx* dGp = dG + nG;
   cplx* dC = dGp + nG;
@@ -1005,7 +1023,6 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   int it = 0, conv = 0;
   for (;; it++) {
     // residuals of every column; W = K_P^{-1} R only for the columns that can receive a search direction
-    const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
     if (!resid_ready) {
       Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + nw));
       ColPtrs X, AX;
@@ -1062,6 +1079,17 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         if (haveP) ccols(sAP, act, T, p + b + na);
         Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * p * 2 * p, 16.0 * len * 2 * p);
         launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
+      } else if (fused_ready) {
+        // the previous update pass left [X W P]^H [W P AP] and (AX)^H W for all nw columns: only
+        // W_a^H A W_a (A W exists since this iteration's apply) is new
+        ColPtrs Wa, AWa;
+        ccols(WW, act, Wa, 0);
+        ccols(AWW, act, AWa, 0);
+        Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * na * na, 16.0 * len * 2 * na);
+        launch_gram(Wa, na, AWa, na, len, dGww, c->gpart.as<cplx>(), st);
+        for (int t = 0; t < na; t++) hAct[t] = act[t];
+        cudaMemcpyAsync(dAct, hAct, na * sizeof(int), cudaMemcpyHostToDevice, st);
+        launch_ug_assemble(dUgRed, b, nw, dAct, na, haveP ? 1 : 0, dGww, dLam, p, dG, st);
       } else {
         // only the blocks that are not known: S^H [W P AW AP]; X^H X = I and X^H A X = Lambda hold for
         // the Ritz vectors X of the previous step, the rest follows by Hermitian symmetry
@@ -1095,7 +1123,20 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       mcols(sAPn, all, Y1a, 0);
       mcols(sAXn, all, Y2a, 0);
       for (int j = nw; j < b; j++) Y1.p[j] = Y1a.p[j] = nullptr;
-      if (c->fuse_resid) {
+      if (ug_ok) {
+        // both updates + the next residual + W + the next iteration's Gram blocks in one pass
+        const UgFlops uf = ug_flops(b, nw);
+        Prof pf(c, PC_STAT_UPDATE, st, 3, 2 * 8.0 * len * p * b + 84.0 * c->n3 * b + uf.flops_per_row * len,
+                16.0 * len * (2 * p + 2 * (b + nw) + nw));
+        MutColPtrs W;
+        mcols(WW, all, W, 0);
+        for (int j = nw; j < b; j++) W.p[j] = nullptr;
+        const int g = launch_update_gram(S, AS, p, dC, p, b, nw, Y2, Y1, Y2a, Y1a, W, dLam, c->n, c->d_ktab,
+                                         c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dUgPart, dUgRed, rg, st);
+        launch_reduce_partial(dPart, g, b, dNorm, st);
+        resid_ready = true;
+        fused_ready = true;
+      } else if (c->fuse_resid) {
         // both updates + the next residual R = AX' - X' Lambda', W = K_P^{-1} R (each row tile's W is
         // read into shared memory by the S phase before the same CTA overwrites it), |R|^2, |X'|^2
         Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + 84.0 * c->n3 * b,

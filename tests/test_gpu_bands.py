@@ -210,3 +210,27 @@ def test_bands_warm_start_path_continuation(api):
         assert rel(warm[0][i], ref) <= 1e-8
         assert rel(cold[0][i], ref) <= 1e-8
     assert warm[2].sum() < cold[2].sum()
+
+
+@pytest.mark.parametrize("opts", [{"fuse_gram": 1}, {"fuse_gram": 1, "w_guard": -1}, {"fuse_resid": 0},
+                                  {"update_tma": 1}, {"gram_refresh": 1}])
+def test_bands_option_variants(api, opts):
+    """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
+    tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""
+    A = synth.lattice("fcc")
+    n = 8
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("fcc_diamond", A, n)
+    k = np.array([PI / 7, 3 * PI / 5, 4 * PI / 13])
+    ctx = api.pc_create(A, n, e, masks)
+    for key, v in opts.items():
+        api.pc_set_option(ctx, key, v)
+    try:
+        r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
+    finally:
+        for key in ("update_tma",):  # process-wide knobs back to their defaults
+            if key in opts:
+                api.pc_set_option(ctx, key, 0)
+    assert r["status"][0] == 0
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    assert rel(r["omega2"][0], O.eigs_dense(op, 10)) <= 1e-8
