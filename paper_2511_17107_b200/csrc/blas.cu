@@ -26,7 +26,10 @@ __global__ void gram_assemble_kernel(const cplx* __restrict__ Gp, const double* 
   if (i < b && j < b) {
     v = (i == j) ? mk(half ? lam[i] : 1.0, 0.0) : mk(0, 0);
   } else if (j >= b) {
-    v = Gp[(size_t)(half * c + (j - b)) * p + i];
+    // [W P]^H [W P] and [W P]^H A [W P] are Hermitian: their strict lower triangles (not computed by
+    // the Gram kernel) are the conjugates of the upper ones
+    if (i >= b && i - b > j - b) v = conjg(Gp[(size_t)(half * c + (i - b)) * p + j]);
+    else v = Gp[(size_t)(half * c + (j - b)) * p + i];
   } else {  // i >= b, j < b: conj of (j, i)
     v = conjg(Gp[(size_t)(half * c + (i - b)) * p + j]);
   }

@@ -74,8 +74,10 @@ void set_gram_ks(int k);  // tuning knob: 1 or 2 warp groups per Gram chunk
 // [G_M | G_A] (p x 2p) from Gp = S^H [W P AW AP] (p x 2c), S = [X W P], b = |X|, c = |W| + |P|,
 // assuming X^H X = I, X^H A X = diag(lambda) (Ritz vectors of the previous Rayleigh-Ritz step).
 void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);
+// hb >= 0: S = [X Y] (|X| = hb), T = [Y AY] (|Y| = hc) with Y^H Y, Y^H A Y Hermitian: 8x8 tiles of their
+// strict lower triangles are skipped (left unwritten in G; launch_gram_assemble mirrors them).
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
-                 cudaStream_t st);
+                 cudaStream_t st, int hb = -1, int hc = 0);
 // Block update (r <= 32 output columns, C column-major ld = ldc):
 //   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr; columns with Y1->p[c] == nullptr skipped)
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])
@@ -88,7 +90,8 @@ void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int s
 // R = AX' - X' diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if deflate0),
 // per-CTA |R_c|^2, |X'_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  r <= 32.  Returns the grid
 // (<= max_grid) for launch_reduce_partial.
-void set_update_tma(int v);  // tuning knob: 1 = bulk-copy (TMA) row tiles, 0 = per-thread cp.async
+void set_update_tma(int v);
+void set_update_compact(int v);  // tuning knob: 1 = update kernel without a shared copy of C (4 CTAs/SM)  // tuning knob: 1 = bulk-copy (TMA) row tiles, 0 = per-thread cp.async
 int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                       const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,

@@ -149,6 +149,7 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
+  int gram_herm = 0;           // 1: skip the strict lower triangles of the Hermitian Gram blocks (measured slower: warp imbalance)
   int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
@@ -444,9 +445,11 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
+  else if (k == "gram_herm") c->gram_herm = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "update_tma") set_update_tma((int)v);
+  else if (k == "update_compact") set_update_compact((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
@@ -1097,7 +1100,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         ccols(AWW, act, T, cw);
         if (haveP) ccols(sAP, act, T, cw + na);
         Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * cw, 16.0 * len * (p + cw));
-        launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st);
+        launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st, c->gram_herm ? b : -1, cw);
         launch_gram_assemble(dGp, dLam, b, cw, dG, st);
       }
       rank = rr(p);

@@ -28,8 +28,11 @@ HD int ua_pitch4mod8(int p) {
 
 // TMA = true: the row tiles arrive by bulk copies (one 256-B run per column and component, issued by
 // warp 0, completion counted on one mbarrier per buffer) instead of per-thread 16-B cp.async.
-template <int NT, bool TMA>
-__global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
+// CPT = true ("compact"): no shared copy of C (its fragments come through the L1 with __ldg) and an
+// unpadded tile pitch of 48 rows with an XOR row swizzle, 55 KB instead of 67 KB of shared memory per
+// CTA: 4 CTAs per SM instead of 3.
+template <int NT, bool TMA, bool CPT>
+__global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 4 : 1) update_all_kernel(
     ColPtrs S, ColPtrs AS, int p, const cplx* __restrict__ C, int ldc, int r, int split, MutColPtrs Y1s,
     MutColPtrs Y2s, MutColPtrs Y1a, MutColPtrs Y2a, MutColPtrs Wout, const double* __restrict__ lam, int n,
     const cplx* __restrict__ kt, double gamma, double thr, int deflate0, double* partial) {
@@ -40,14 +43,19 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   const int n3 = n * n * n;
   const int pe = (p + 3) & ~3;
   const int PS = ua_pitch4mod8(pe);
-  cplx* Buf = reinterpret_cast<cplx*>(uasm);  // [2][pe][UA_RP]: buffer 0 = S tiles, 1 = AS tiles
-  cplx* Cs = Buf + 2 * pe * UA_RP;            // [NT*8][PS]
+  constexpr int RP = CPT ? UA_ROWS : UA_RP;
+  static_assert(!(TMA && CPT), "bulk copies need the unswizzled layout");
+  // tile element (column m, row rho): CPT swizzles rows within aligned groups of 8 so that the four
+  // columns of an A fragment (m & 3 = 0..3) land in distinct banks despite the 48-row pitch
+  auto RI = [](int m, int rho) { return m * RP + (CPT ? (rho ^ (2 * (m & 3))) : rho); };
+  cplx* Buf = reinterpret_cast<cplx*>(uasm);  // [2][pe][RP]: buffer 0 = S tiles, 1 = AS tiles
+  cplx* Cs = Buf + 2 * pe * RP;               // [NT*8][PS] (not with CPT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rg = warp & 1, ng = warp >> 1;
 
   for (int e = tid; e < NT * 8 * pe; e += UA_THREADS) {
     int c = e / pe, m = e % pe;
-    Cs[c * PS + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
+    if (!CPT) Cs[c * PS + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
   }
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
   const cplx* dummy = S.p[0];
@@ -67,7 +75,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
   }
   auto load_tile = [&](int buf, const ColPtrs& src, long long t) {
     const long long m0 = t * UA_SEG;
-    cplx* dst = Buf + buf * pe * UA_RP;
+    cplx* dst = Buf + buf * pe * RP;
     if constexpr (TMA) {
       if (warp == 0) {
         const int nv = (int)min((long long)UA_SEG, (long long)n3 - m0);
@@ -87,7 +95,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
       const int seg = rho / UA_SEG, rr = rho % UA_SEG;
       const long long mode = m0 + rr;
       const bool ok = (m < p) && (mode < n3);
-      cp_async16_zfill(&dst[m * UA_RP + rho],
+      cp_async16_zfill(&dst[RI(m, rho)],
                        ok ? (const void*)(src.p[m] + (long long)seg * n3 + mode) : (const void*)dummy, ok);
     }
     cp_async_commit();
@@ -114,13 +122,19 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
       const bool in = (mm >= mlo) && (mm < mhi);
       cplx a[3];
 #pragma unroll
-      for (int s = 0; s < 3; s++) a[s] = Sc[mm * UA_RP + s * UA_SEG + lrow];
+      for (int s = 0; s < 3; s++) a[s] = Sc[RI(mm, s * UA_SEG + lrow)];
 #pragma unroll
       for (int i = 0; i < NTW; i++) {
         const int nt = ng + 2 * i;
         if (nt >= NT) break;
-        cplx cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
-        if (!in) cv = mk(0, 0);
+        cplx cv;
+        if constexpr (CPT) {
+          const int cc = nt * 8 + (lane >> 2);
+          cv = (in && cc < r) ? ldg(C + (size_t)cc * ldc + mm) : mk(0, 0);
+        } else {
+          cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
+          if (!in) cv = mk(0, 0);
+        }
         const double cs = cv.x + cv.y;
 #pragma unroll
         for (int s = 0; s < 3; s++) {
@@ -188,7 +202,7 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
       __syncthreads();
     }
     zero();
-    const cplx* Ac = Buf + pe * UA_RP;
+    const cplx* Ac = Buf + pe * RP;
     kloop(Ac, split, p);
     store(Y1a, false);
     kloop(Ac, 0, split);
@@ -265,24 +279,30 @@ __global__ void __launch_bounds__(UA_THREADS) update_all_kernel(
 static int g_update_tma = 0;  // pc_set_option "update_tma": 1 = bulk copies (measured slower: 256-B runs)
 void set_update_tma(int v) { g_update_tma = v ? 1 : 0; }
 
-template <int NT, bool TMA>
+static int g_update_cpt = 0;  // pc_set_option "update_compact": 1 = CPT kernel (4 CTAs per SM; measured slower)
+void set_update_compact(int v) { g_update_cpt = v ? 1 : 0; }
+
+template <int NT, bool TMA, bool CPT>
 static int run_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                           const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a,
                           const MutColPtrs& Y2a, const MutColPtrs& W, const double* lam, int n, const cplx* kt,
                           double gamma, double thr, int deflate0, double* partial, int max_grid, cudaStream_t st) {
   const int pe = (p + 3) & ~3, ps = ua_pitch4mod8(pe);
-  const size_t smem = (size_t)(2 * pe * UA_RP + NT * 8 * ps) * sizeof(cplx);
+  const size_t smem = (size_t)(2 * pe * (CPT ? UA_ROWS : UA_RP) + (CPT ? 0 : NT * 8 * ps)) * sizeof(cplx);
+  auto kern = update_all_kernel<NT, TMA, CPT>;
   static bool attr = false;
   if (!attr) {
-    cudaFuncSetAttribute(update_all_kernel<NT, TMA>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
     attr = true;
   }
+  int occ = 0;
+  cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, UA_THREADS, smem);
+  occ = std::max(1, std::min(8, occ));
   const long long n3 = (long long)n * n * n;
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
-  const int occ = std::max(1, std::min(8, (int)((227 * 1024) / (smem + 2048))));
   const int grid = (int)std::min<long long>(std::min<long long>(ntiles, 148LL * occ), max_grid);
-  update_all_kernel<NT, TMA><<<grid, UA_THREADS, smem, st>>>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n,
-                                                         kt, gamma, thr, deflate0, partial);
+  kern<<<grid, UA_THREADS, smem, st>>>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr,
+                                       deflate0, partial);
   return grid;
 }
 
@@ -290,14 +310,15 @@ int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C,
                       const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
                       int deflate0, double* partial, int max_grid, cudaStream_t st) {
-#define PC_UA(NT_)                                                                                                \
-  return g_update_tma ? run_update_all<NT_, true>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt,     \
-                                                  gamma, thr, deflate0, partial, max_grid, st)                     \
-                      : run_update_all<NT_, false>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr, deflate0, \
-                             partial, max_grid, st)
+#define PC_UA_ARGS S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr, deflate0, partial, max_grid, st
+#define PC_UA(NT_)                                                 \
+  return g_update_tma ? run_update_all<NT_, true, false>(PC_UA_ARGS) \
+         : g_update_cpt ? run_update_all<NT_, false, true>(PC_UA_ARGS) \
+                        : run_update_all<NT_, false, false>(PC_UA_ARGS)
   if (r <= 8) PC_UA(1);
   if (r <= 16) PC_UA(2);
   if (r <= 24) PC_UA(3);
   PC_UA(4);
 #undef PC_UA
+#undef PC_UA_ARGS
 }

@@ -23,7 +23,10 @@ struct XRow {
 
 template <int N>
 struct XexCfg {
-  static constexpr int TP = pow2_div(N, 8);   // output rows per tile
+#ifndef PC_XEX_TP
+#define PC_XEX_TP 8
+#endif
+  static constexpr int TP = pow2_div(N, PC_XEX_TP);   // output rows per tile
   static constexpr int RP = TP + 2;           // rows held (1 halo row each side)
   static constexpr int P = XRow<N>::P;        // row pitch in complex
   static constexpr int NT = 256;

@@ -213,7 +213,8 @@ def test_bands_warm_start_path_continuation(api):
 
 
 @pytest.mark.parametrize("opts", [{"fuse_gram": 1}, {"fuse_gram": 1, "w_guard": -1}, {"fuse_resid": 0},
-                                  {"update_tma": 1}, {"gram_refresh": 1}])
+                                  {"update_tma": 1}, {"gram_refresh": 1}, {"gram_herm": 1},
+                                  {"update_compact": 1}])
 def test_bands_option_variants(api, opts):
     """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
     tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""
@@ -228,7 +229,7 @@ def test_bands_option_variants(api, opts):
     try:
         r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
     finally:
-        for key in ("update_tma",):  # process-wide knobs back to their defaults
+        for key in ("update_tma", "update_compact"):  # process-wide knobs back to their defaults
             if key in opts:
                 api.pc_set_option(ctx, key, 0)
     assert r["status"][0] == 0

@@ -5,8 +5,8 @@ for spec in "$@"; do
   name=${spec%%:*}; flags=${spec#*:}
   make -j16 BUILD=build/$name LIB=build/$name/libpcband.so EXTRA="$flags" >/dev/null 2>&1 || echo "build $name failed"
 done
-echo "default $(python tools/pass_time.py)"
+echo "default $(python tools/apply_time.py C4 15)"
 for spec in "$@"; do
   name=${spec%%:*}
-  echo "$name $(PCBAND_LIB=$PWD/build/$name/libpcband.so python tools/pass_time.py)"
+  echo "$name $(PCBAND_LIB=$PWD/build/$name/libpcband.so python tools/apply_time.py C4 15)"
 done
