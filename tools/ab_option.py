@@ -22,6 +22,7 @@ ap.add_argument("--key", required=True)
 ap.add_argument("--values", type=float, nargs="+", required=True)
 ap.add_argument("--nk", type=int, default=2)
 ap.add_argument("--tol", type=float, default=1e-5)
+ap.add_argument("--maxit", type=int, default=1000)
 a = ap.parse_args()
 W = synth.WORKLOADS[a.workload]
 A = W.A()
@@ -36,7 +37,7 @@ for v in a.values:
     api.pc_stats(ctx, reset=True)
     torch.cuda.synchronize()
     t = time.time()
-    r = api.pc_bands(ctx, kp, nev=W.nev, tol=a.tol, maxit=1000)
+    r = api.pc_bands(ctx, kp, nev=W.nev, tol=a.tol, maxit=a.maxit)
     torch.cuda.synchronize()
     el = time.time() - t
     st = api.pc_stats(ctx)
