@@ -562,17 +562,17 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
     // Middle passes (y-inverse, x-inverse + M_eps + x-forward, y-forward) in L2-sized chunks of
     // (column, z-planes): the chunk written by one pass is re-read by the next while it is still in
     // the 126 MB L2, so HBM only sees the first read of u and the final write-back of s.
+    // A chunk is a slab of z-planes of ALL nc columns (so each launch still fills the GPU), sized so
+    // that the slab (chunk_mb per buffer) stays in L2 between the three passes.
     const double chunk_bytes = c->chunk_mb * 1048576.0;
-    const double plane_bytes = 3.0 * n * n * sizeof(cplx);  // one z-plane, 3 components, one column
+    const double plane_bytes = 3.0 * n * n * sizeof(cplx) * nc;  // one z-plane, 3 components, nc columns
     int nzc = n;
     if (c->chunk_mb > 0) {
       nzc = (int)std::max(1.0, std::floor(chunk_bytes / plane_bytes));
       while (nzc < n && n % nzc) nzc--;  // divisor of n
       nzc = std::min(nzc, n);
     }
-    const int ccols = (nzc == n && c->chunk_mb > 0)
-                          ? std::max(1, std::min(nc, (int)std::floor(chunk_bytes / (plane_bytes * n))))
-                          : (c->chunk_mb > 0 ? 1 : nc);
+    const int ccols = nc;
     for (int j0 = 0; j0 < nc; j0 += ccols) {
       const int cn = std::min(ccols, nc - j0);
       ColPtrs Ys, Ws;

@@ -14,6 +14,9 @@ ncol = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 A = W.A()
 masks = synth.make_masks(W.geometry, A, W.n)
 ctx = api.pc_create(A, W.n, W.eps1(), masks)
+for kv in sys.argv[3:]:  # extra key=value options
+    key, v = kv.split("=")
+    api.pc_set_option(ctx, key, float(v))
 X = torch.randn(ncol, 3 * W.n ** 3, dtype=torch.complex128, device="cuda")
 Y = torch.empty_like(X)
 k = W.kpoints()[5]
