@@ -214,6 +214,12 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
   G[idx] = acc;
 }
 
+#ifndef PC_GRAM40_KC  // rows per pipeline chunk / stages of the 40 x 40 Gram block (the C4 bench shape)
+#define PC_GRAM40_KC 16
+#endif
+#ifndef PC_GRAM40_ST
+#define PC_GRAM40_ST 3
+#endif
 static int g_gram_ks = 2;  // pc_set_option "gram_ks" (1 or 2), process-wide tuning knob
 void set_gram_ks(int k) { g_gram_ks = (k == 1) ? 1 : 2; }
 
@@ -276,7 +282,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     case 1: PC_GRAM_CASE(3, 2, 2, 3, 16, 3) break;
     case 2: PC_GRAM_CASE(2, 2, 2, 4, 16, 3) break;
     case 3: PC_GRAM_CASE(2, 2, 2, 2, 16, 3) break;
-    case 4: PC_GRAM_CASE(5, 1, 1, 5, 16, 3) break;
+    case 4: PC_GRAM_CASE(5, 1, 1, 5, PC_GRAM40_KC, PC_GRAM40_ST) break;
     case 5: PC_GRAM_CASE(5, 1, 1, 8, 16, 3) break;
     case 6: PC_GRAM_CASE(4, 2, 2, 4, 16, 3) break;
     case 7: PC_GRAM_CASE(5, 2, 2, 4, 16, 3) break;
