@@ -149,6 +149,7 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
+  int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
   int gram_herm = 0;           // 1: skip the strict lower triangles of the Hermitian Gram blocks (measured slower: warp imbalance)
   int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
@@ -446,6 +447,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
   else if (k == "gram_herm") c->gram_herm = (int)v;
+  else if (k == "trim_locked") c->trim_locked = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "update_tma") set_update_tma((int)v);
@@ -1024,6 +1026,11 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   c->hist_b = b;
   bool haveP = false, resid_ready = false;
   int it = 0, conv = 0;
+  // trim_locked: the update writes W', P', AP' only for the columns that are active in this iteration
+  // (soft-locked columns skip 3 column writes each).  A locked column that re-activates (sticky_lock = 0)
+  // gets its W from one residual pass and enters without a P column.
+  const bool trim = c->trim_locked && !ug_ok;
+  std::vector<char> hasW(b, 0), hasP(b, 0);
   for (;; it++) {
     // residuals of every column; W = K_P^{-1} R only for the columns that can receive a search direction
     if (!resid_ready) {
@@ -1035,6 +1042,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       mcols(WW, all, W, 0);
       for (int j = nw; j < b; j++) W.p[j] = nullptr;
       launch_resid(X, AX, W, dLam, b, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dNorm, st);
+      for (int j = 0; j < b; j++) hasW[j] = j < nw;
     }
     cudaMemcpyAsync(hN, dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
     {
@@ -1065,21 +1073,38 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (active[j]) act.push_back(j);
     const int na = (int)act.size();
     if (na == 0) break;
+    std::vector<int> actP, miss;
+    for (int j : act) {
+      if (!trim || hasP[j]) actP.push_back(j);
+      if (!hasW[j]) miss.push_back(j);
+    }
+    if (!miss.empty()) {  // re-activated columns: W = K_P^{-1} (AX - X Lambda) for them only
+      Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + (double)miss.size()));
+      ColPtrs X, AX;
+      MutColPtrs W;
+      ccols(sX, all, X, 0);
+      ccols(sAX, all, AX, 0);
+      for (int j = 0; j < b; j++) W.p[j] = nullptr;
+      for (int j : miss) W.p[j] = col(WW, j);
+      launch_resid(X, AX, W, dLam, b, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dNorm, st);
+      for (int j : miss) hasW[j] = 1;
+    }
+    const int nP = (int)actP.size();
     CHK(apply_list(WW, AWW, act));
     int p = 0;
     for (int attempt = 0; attempt < 2; attempt++) {
-      p = b + na + (haveP ? na : 0);
+      p = b + na + (haveP ? nP : 0);
       const int cw = p - b;  // |W| + |P|
       ColPtrs S, T;
       ccols(sX, all, S, 0);
       ccols(WW, act, S, b);
-      if (haveP) ccols(sP, act, S, b + na);
+      if (haveP) ccols(sP, actP, S, b + na);
       const bool full = c->gram_refresh > 0 && (it % c->gram_refresh) == c->gram_refresh - 1;
       if (full) {  // periodic full Gram S^H [S AS]: no assumption on X (guards against drift)
         for (int t = 0; t < p; t++) T.p[t] = S.p[t];
         ccols(sAX, all, T, p);
         ccols(AWW, act, T, p + b);
-        if (haveP) ccols(sAP, act, T, p + b + na);
+        if (haveP) ccols(sAP, actP, T, p + b + na);
         Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * p * 2 * p, 16.0 * len * 2 * p);
         launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
       } else if (fused_ready) {
@@ -1098,7 +1123,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         // the Ritz vectors X of the previous step, the rest follows by Hermitian symmetry
         for (int t = 0; t < cw; t++) T.p[t] = S.p[b + t];
         ccols(AWW, act, T, cw);
-        if (haveP) ccols(sAP, act, T, cw + na);
+        if (haveP) ccols(sAP, actP, T, cw + na);
         Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * cw, 16.0 * len * (p + cw));
         launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st, c->gram_herm ? b : -1, cw);
         launch_gram_assemble(dGp, dLam, b, cw, dG, st);
@@ -1117,15 +1142,24 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       MutColPtrs Y1, Y2, Y1a, Y2a;
       ccols(sX, all, S, 0);
       ccols(WW, act, S, b);
-      if (haveP) ccols(sP, act, S, b + na);
+      if (haveP) ccols(sP, actP, S, b + na);
       ccols(sAX, all, AS, 0);
       ccols(AWW, act, AS, b);
-      if (haveP) ccols(sAP, act, AS, b + na);
+      if (haveP) ccols(sAP, actP, AS, b + na);
       mcols(sPn, all, Y1, 0);
       mcols(sXn, all, Y2, 0);
       mcols(sAPn, all, Y1a, 0);
       mcols(sAXn, all, Y2a, 0);
-      for (int j = nw; j < b; j++) Y1.p[j] = Y1a.p[j] = nullptr;
+      std::vector<char> wr(b, 0);  // columns that get W', P', AP' from this update
+      for (int j = 0; j < nw; j++) wr[j] = 1;
+      if (trim) {
+        for (int j = 0; j < b; j++) wr[j] = 0;
+        for (int j : act) wr[j] = 1;
+      }
+      for (int j = 0; j < b; j++) {
+        if (!wr[j]) Y1.p[j] = Y1a.p[j] = nullptr;
+        hasP[j] = wr[j];
+      }
       if (ug_ok) {
         // both updates + the next residual + W + the next iteration's Gram blocks in one pass
         const UgFlops uf = ug_flops(b, nw);
@@ -1134,6 +1168,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         MutColPtrs W;
         mcols(WW, all, W, 0);
         for (int j = nw; j < b; j++) W.p[j] = nullptr;
+        for (int j = 0; j < b; j++) hasW[j] = j < nw;
         const int g = launch_update_gram(S, AS, p, dC, p, b, nw, Y2, Y1, Y2a, Y1a, W, dLam, c->n, c->d_ktab,
                                          c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dUgPart, dUgRed, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
@@ -1146,7 +1181,10 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
                 16.0 * len * (2 * p + 2 * (b + nw) + nw));
         MutColPtrs W;
         mcols(WW, all, W, 0);
-        for (int j = nw; j < b; j++) W.p[j] = nullptr;
+        for (int j = 0; j < b; j++) {
+          if (!wr[j]) W.p[j] = nullptr;
+          hasW[j] = wr[j];
+        }
         const int g = launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
                                         c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
