@@ -90,6 +90,11 @@ void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int s
 // R = AX' - X' diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if deflate0),
 // per-CTA |R_c|^2, |X'_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  r <= 32.  Returns the grid
 // (<= max_grid) for launch_reduce_partial.
+// Same contract as launch_update_all, barrier-free streaming kernel (update_stream.cu).
+int launch_update_stream(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
+                         const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
+                         const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
+                         int deflate0, double* partial, int max_grid, cudaStream_t st);
 void set_update_tma(int v);
 void set_update_compact(int v);  // tuning knob: 1 = update kernel without a shared copy of C (4 CTAs/SM)  // tuning knob: 1 = bulk-copy (TMA) row tiles, 0 = per-thread cp.async
 int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,

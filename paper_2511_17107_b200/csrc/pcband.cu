@@ -149,6 +149,7 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
+  int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
   int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
   int gram_herm = 0;           // 1: skip the strict lower triangles of the Hermitian Gram blocks (measured slower: warp imbalance)
   int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
@@ -448,6 +449,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
   else if (k == "gram_herm") c->gram_herm = (int)v;
   else if (k == "trim_locked") c->trim_locked = (int)v;
+  else if (k == "update_stream") c->update_stream = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "update_tma") set_update_tma((int)v);
@@ -1185,8 +1187,11 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
           if (!wr[j]) W.p[j] = nullptr;
           hasW[j] = wr[j];
         }
-        const int g = launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
-                                        c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+        const int g = c->update_stream
+                          ? launch_update_stream(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                                 c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st)
+                          : launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                              c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
         resid_ready = true;
       } else {
