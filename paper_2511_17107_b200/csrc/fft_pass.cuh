@@ -116,8 +116,16 @@ struct TileMap {
 // Persistent, double-buffered pass: CTA b processes tiles b, b + G, b + 2G, ...; the next tile streams
 // into the other shared-memory stage (cp.async) while the current one is transformed and written.
 // Tile index t -> (tile in volume t % TPV, column/component t / TPV).
+#ifndef PC_FFT_BOUNDS
+#define PC_FFT_BOUNDS 0  // 1: min-blocks launch bounds (4 CTAs/SM for the symbol passes, 3 for the plain ones)
+#endif
+#if PC_FFT_BOUNDS
+#define PC_FFT_LB(OP_, ...) __launch_bounds__((__VA_ARGS__), (OP_) != OP_NONE ? 4 : 3)
+#else
+#define PC_FFT_LB(OP_, ...) __launch_bounds__((__VA_ARGS__))
+#endif
 template <int N, int AXIS, int DIR, int OP, int C>
-__global__ void __launch_bounds__(TileCfg<N, C>::NT)
+__global__ void PC_FFT_LB(OP, TileCfg<N, C>::NT)
 fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) {
   constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
   static_assert(R1 * R2 == N, "bad plan");
