@@ -171,6 +171,14 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  its residual rises above tol again
  *   "gram_refresh" every n-th iteration forms the full Gram matrices instead of using
  *                  X^H X = I, X^H A X = Lambda (default 16; 0 = never)
+ *   "gram_derive"  1: the X^H P, P^H P, X^H A P, P^H A P blocks of the Rayleigh-Ritz Gram come from
+ *                  the previous step's Gram and Ritz coefficients (P = S0 C0P), so only S^H [W AW] is
+ *                  formed from the vectors (15 % less Gram time at n=128, but numerically unstable
+ *                  near convergence on degenerate spectra); 0 (default): S^H [W P AW AP] from the vectors
+ *   "derive_tau"   cancellation factor sum|C0P||G0||C0P| / |P^H (.) P| above which a derived Gram is
+ *                  rejected and formed from the vectors instead (default 1e5)
+ *   "xdev_tol"     if max_j | |X_j|^2 - 1 | exceeds this, the next Gram is formed in full from the
+ *                  vectors (default 1e-10)
  *   "p_restart"    1 (default): drop the P block when the basis is numerically rank deficient
  *   "verbose"      1: per-iteration residuals on stderr
  *   "warm_start"   1: start each k-point (k != 0) from the Ritz block of the previous pc_bands

@@ -256,7 +256,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
                  cudaStream_t st, int hb, int hc) {
   struct Opt { int bm, bn; };
   const Opt opts[] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}, {40, 40}, {40, 64}, {64, 64}, {80, 64},
-                      {80, 96}, {24, 32}, {48, 96}};
+                      {80, 96}, {24, 32}, {48, 96}, {40, 24}};
   const int nopt = sizeof(opts) / sizeof(opts[0]);
   int best = 0;
   double best_cost = 1e300;
@@ -288,6 +288,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     case 7: PC_GRAM_CASE(5, 2, 2, 4, 16, 3) break;
     case 8: PC_GRAM_CASE(5, 3, 2, 4, 16, 2) break;
     case 9: PC_GRAM_CASE(3, 1, 1, 4, 16, 3) break;
+    case 11: PC_GRAM_CASE(5, 1, 1, 3, 16, 3) break;
     default: PC_GRAM_CASE(3, 3, 2, 4, 16, 3) break;
   }
 }

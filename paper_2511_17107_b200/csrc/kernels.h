@@ -74,6 +74,13 @@ void set_gram_ks(int k);  // tuning knob: 1 or 2 warp groups per Gram chunk
 // [G_M | G_A] (p x 2p) from Gp = S^H [W P AW AP] (p x 2c), S = [X W P], b = |X|, c = |W| + |P|,
 // assuming X^H X = I, X^H A X = diag(lambda) (Ritz vectors of the previous Rayleigh-Ritz step).
 void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);
+// [G_M | G_A] (p x 2p, p = b + na + nP) of S = [X W_a P_a] from Gw = S^H [W_a AW_a] (p x 2na, ld p) and
+// the P blocks derived from the previous step: G0 (p0 x 2p0, the Gram its Rayleigh-Ritz used), C0
+// (p0 x b, ld p0, its Ritz coefficients), actP (device, nP ints) = the P columns kept.  *cancel (device)
+// = max over P columns and both Grams of sum|C0P||G0||C0P| / |P^H (.) P| (the cancellation factor of
+// the derived entries).  Returns -1 if the sizes are out of range (nothing launched).
+int launch_gram_derive(const cplx* G0, int p0, const cplx* C0, const int* actP, int nP, const cplx* Gw, int na,
+                       const double* lam, int b, cplx* G, double* cancel, cudaStream_t st);
 // hb >= 0: S = [X Y] (|X| = hb), T = [Y AY] (|Y| = hc) with Y^H Y, Y^H A Y Hermitian: 8x8 tiles of their
 // strict lower triangles are skipped (left unwritten in G; launch_gram_assemble mirrors them).
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,

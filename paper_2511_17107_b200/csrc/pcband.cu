@@ -151,6 +151,10 @@ struct pc_ctx {
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
   int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
+  int gram_derive = 0;         // 1: P blocks of the Gram from the previous Gram and Ritz coefficients (see solve_k; unstable)
+  double derive_tau = 1e5;     // ... unless their cancellation factor exceeds this (then from the vectors)
+  double xdev_tol = 1e-10;     // max | |X_j|^2 - 1 | above which the next Gram is formed in full
+  int derive_fallbacks = 0;    // iterations of the last solve whose derived Gram was rejected
   int gram_herm = 0;           // 1: skip the strict lower triangles of the Hermitian Gram blocks (measured slower: warp imbalance)
   int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
@@ -449,6 +453,9 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
   else if (k == "gram_herm") c->gram_herm = (int)v;
   else if (k == "trim_locked") c->trim_locked = (int)v;
+  else if (k == "gram_derive") c->gram_derive = (int)v;
+  else if (k == "derive_tau") c->derive_tau = v;
+  else if (k == "xdev_tol") c->xdev_tol = v;
   else if (k == "update_stream") c->update_stream = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
@@ -915,7 +922,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   // small device buffers: G (maxp x 2maxp), C (maxp x b), lam, info, rr scratch, resid partials, norms
   const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)3 * 80 * 80;
   const int rg = resid_grid(c->n);
-  size_t small_bytes = (2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) + 64;
+  size_t small_bytes = (3 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2 + 2) * sizeof(double) +
+                       (size_t)(8 + maxp) * sizeof(int) + 64;
   CHK(c->small.ensure(small_bytes));
   CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
   // fused update + next-iteration Gram (update_gram.cu): only the first nw columns ever get W and P
@@ -933,14 +941,25 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     dAct = reinterpret_cast<int*>(dGww + b * b);
   }
   bool fused_ready = false;  // dUgRed holds the Gram blocks of the current [X W P] (all nw W, P columns)
-  cplx* dG = c->small.as<cplx>();
-  cplx* dGp = dG + nG;
+  // two Gram buffers: the Rayleigh-Ritz of an iteration reads one, the next iteration's derived P blocks
+  // (option gram_derive) read it while the new Gram is assembled into the other
+  cplx* const dGbuf[2] = {c->small.as<cplx>(), c->small.as<cplx>() + nG};
+  cplx* dG = dGbuf[0];
+  cplx* dGp = dGbuf[1] + nG;
   cplx* dC = dGp + nG;
   cplx* dScr = dC + nC;
   double* dLam = reinterpret_cast<double*>(dScr + nScr);
   double* dNorm = dLam + b;
   double* dPart = dNorm + 2 * b;
-  int* dInfo = reinterpret_cast<int*>(dPart + (size_t)rg * b * 2);
+  double* dCancel = dPart + (size_t)rg * b * 2;
+  int* dInfo = reinterpret_cast<int*>(dCancel + 2);
+  int* dActP = dInfo + 8;
+  int* hActP = reinterpret_cast<int*>(c->h_pinned + 3584);
+  double* hCancel = c->h_pinned + 3700;
+  double last_cancel = 0.0;
+  bool force_full = false;  // next Gram from the vectors in full (X^H X = I no longer trusted)
+  int p_prev = 0;          // size of the basis of the last Rayleigh-Ritz (dG, dC hold its Gram and C)
+  bool g_prev = false;     // dG / dC describe the basis that produced the current X and P
   double* hN = c->h_pinned;                 // 2b norms
   int* hInfo = reinterpret_cast<int*>(c->h_pinned + 2048);
   MutColPtrs wsp;
@@ -1027,6 +1046,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   c->hist.clear();
   c->hist_b = b;
   bool haveP = false, resid_ready = false;
+  c->derive_fallbacks = 0;
   int it = 0, conv = 0;
   // trim_locked: the update writes W', P', AP' only for the columns that are active in this iteration
   // (soft-locked columns skip 3 column writes each).  A locked column that re-activates (sticky_lock = 0)
@@ -1053,6 +1073,9 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     }
     if (c->profile) prof_flush(c);
     conv = 1;
+    double xdev = 0.0;  // X^H X = I is assumed by the Gram assembly; its diagonal is measured here
+    for (int j = 0; j < b; j++) xdev = std::max(xdev, std::fabs(hN[2 * j + 1] - 1.0));
+    force_full = !(xdev <= c->xdev_tol);
     for (int j = 0; j < b; j++) {
       res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
       c->hist.push_back(res[j]);
@@ -1062,13 +1085,15 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       else if (!c->sticky_lock) active[j] = 1;
       // guard columns beyond nev + w_guard never get a search direction (they ride along in X and P)
       if (c->w_guard >= 0 && j >= nev + c->w_guard) active[j] = 0;
-      if (j < nev && res[j] > tol) conv = 0;
+      if (j < nev && !(res[j] <= tol)) conv = 0;
     }
     if (c->verbose) {
-      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d res:", kidx, it, rank, hInfo[2], hInfo[1]);
+      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d |X|-1 %.1e cancel %.1e fb %d res:", kidx, it,
+              rank, hInfo[2], hInfo[1], xdev, last_cancel, c->derive_fallbacks);
       for (int j = 0; j < b; j++) fprintf(stderr, " %.2e%s", res[j], active[j] ? "" : "*");
       fprintf(stderr, "\n");
     }
+    if (force_full && it < maxit) conv = 0;  // Ritz pairs not trusted: one more step with a full Gram
     if (conv || it >= maxit) break;
     std::vector<int> act;
     for (int j = 0; j < b; j++)
@@ -1094,14 +1119,17 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     const int nP = (int)actP.size();
     CHK(apply_list(WW, AWW, act));
     int p = 0;
-    for (int attempt = 0; attempt < 2; attempt++) {
+    cplx* const dG0 = dG;  // the previous step's Gram (read by the derived assembly)
+    dG = (dG == dGbuf[0]) ? dGbuf[1] : dGbuf[0];
+    for (int attempt = 0, pass = 0; attempt < 2; attempt++) {
       p = b + na + (haveP ? nP : 0);
       const int cw = p - b;  // |W| + |P|
       ColPtrs S, T;
       ccols(sX, all, S, 0);
       ccols(WW, act, S, b);
       if (haveP) ccols(sP, actP, S, b + na);
-      const bool full = c->gram_refresh > 0 && (it % c->gram_refresh) == c->gram_refresh - 1;
+      const bool full = force_full || (c->gram_refresh > 0 && (it % c->gram_refresh) == c->gram_refresh - 1);
+      bool used_derive = false;
       if (full) {  // periodic full Gram S^H [S AS]: no assumption on X (guards against drift)
         for (int t = 0; t < p; t++) T.p[t] = S.p[t];
         ccols(sAX, all, T, p);
@@ -1120,6 +1148,24 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         for (int t = 0; t < na; t++) hAct[t] = act[t];
         cudaMemcpyAsync(dAct, hAct, na * sizeof(int), cudaMemcpyHostToDevice, st);
         launch_ug_assemble(dUgRed, b, nw, dAct, na, haveP ? 1 : 0, dGww, dLam, p, dG, st);
+      } else if (c->gram_derive && haveP && g_prev && nP > 0 && pass == 0 &&
+                 b + na + nP <= 80 && p_prev <= 80) {
+        // S^H [W AW] from the vectors; X^H P, P^H P, X^H AP, P^H AP from the previous Gram and Ritz
+        // coefficients (P = S0 C0P, X = S0 C0); X^H X = I, X^H A X = Lambda as below
+        ColPtrs T;
+        ccols(WW, act, T, 0);
+        ccols(AWW, act, T, na);
+        {
+          Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * na, 16.0 * len * (p + na));
+          launch_gram(S, p, T, 2 * na, len, dGp, c->gpart.as<cplx>(), st);
+        }
+        for (int t = 0; t < nP; t++) hActP[t] = actP[t];
+        cudaMemcpyAsync(dActP, hActP, nP * sizeof(int), cudaMemcpyHostToDevice, st);
+        c->launches += 1;
+        if (launch_gram_derive(dG0, p_prev, dC, dActP, nP, dGp, na, dLam, b, dG, dCancel, st) != 0)
+          return set_err(PC_EINVAL, "gram_derive: sizes out of range");
+        cudaMemcpyAsync(hCancel, dCancel, sizeof(double), cudaMemcpyDeviceToHost, st);
+        used_derive = true;
       } else {
         // only the blocks that are not known: S^H [W P AW AP]; X^H X = I and X^H A X = Lambda hold for
         // the Ritz vectors X of the previous step, the rest follows by Hermitian symmetry
@@ -1131,6 +1177,20 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         launch_gram_assemble(dGp, dLam, b, cw, dG, st);
       }
       rank = rr(p);
+      if (used_derive) {
+        last_cancel = *hCancel;
+        if (!(last_cancel <= c->derive_tau)) {
+          // the derived P blocks lost too many digits to cancellation: form this Gram from the vectors
+          // (the Rayleigh-Ritz above is discarded; dG0 and dC of the previous step are not needed again)
+          c->derive_fallbacks += 1;
+          pass = 1;
+          attempt--;
+          continue;
+        }
+      }
+      pass = 0;
+      p_prev = p;
+      g_prev = true;
       if (rank >= p || (rank >= b && !c->p_restart)) break;
       if (rank >= b && !haveP) break;
       if (!haveP) return set_err(PC_ENUMERIC, "pc_bands: Rayleigh-Ritz basis collapsed (rank " +

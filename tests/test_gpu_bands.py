@@ -215,7 +215,7 @@ def test_bands_warm_start_path_continuation(api):
 @pytest.mark.parametrize("opts", [{"fuse_gram": 1}, {"fuse_gram": 1, "w_guard": -1}, {"fuse_resid": 0},
                                   {"update_tma": 1}, {"gram_refresh": 1}, {"gram_herm": 1},
                                   {"update_compact": 1}, {"trim_locked": 0}, {"sticky_lock": 1},
-                                  {"update_stream": 1}])
+                                  {"update_stream": 1}, {"gram_derive": 1}])
 def test_bands_option_variants(api, opts):
     """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
     tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""
