@@ -60,6 +60,7 @@ def lib():
         "pc_debug_heevj": (i, [dp, i, dp, dp, ip]),
         "pc_debug_pass": (i, [vp, dp, i, i, i, vp, vp, vp, i, ll, d]),
         "pc_history": (i, [vp, dp, i, ip]),
+        "pc_bench_block": (i, [vp, i, i, i, i, i, dp]),
         "pc_destroy": (None, [vp]),
         "pc_trim": (None, [i]),
         "pc_last_error": (ctypes.c_char_p, []),
@@ -226,6 +227,13 @@ def pc_history(ctx: Ctx):
     out = np.zeros(max(1, rows * b.value))
     lib().pc_history(ctx.h, _dptr(out), rows, ctypes.byref(b))
     return out[: rows * b.value].reshape(rows, b.value)
+
+
+def pc_bench_block(ctx: Ctx, which: int, b: int, na: int, nP: int, reps: int = 10) -> float:
+    """Mean milliseconds of one LOBPCG block-kernel launch group on random data (timing only)."""
+    ms = ctypes.c_double()
+    _check(lib().pc_bench_block(ctx.h, int(which), int(b), int(na), int(nP), int(reps), ctypes.byref(ms)))
+    return ms.value
 
 
 def pc_trim(device=-1):

@@ -220,6 +220,10 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
 #ifndef PC_GRAM40_ST
 #define PC_GRAM40_ST 3
 #endif
+static double g_grid_frac = 1.0;
+void set_grid_frac(double f) { g_grid_frac = (f > 0.0 && f <= 1.0) ? f : 1.0; }
+int grid_cap(int ctas_per_sm) { return std::max(1, (int)(g_grid_frac * 148.0 * ctas_per_sm + 0.5)); }
+
 static int g_gram_ks = 2;  // pc_set_option "gram_ks" (1 or 2), process-wide tuning knob
 void set_gram_ks(int k) { g_gram_ks = (k == 1) ? 1 : 2; }
 
@@ -239,7 +243,7 @@ static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long
   }
   const int nmb = (p + Cfg::BM - 1) / Cfg::BM, nnb = (q + Cfg::BN - 1) / Cfg::BN;
   const int nblk = nmb * nnb;
-  int ns = std::max(1, (ctas_per_sm * 148 + nblk - 1) / nblk);
+  int ns = std::max(1, (grid_cap(ctas_per_sm) + nblk - 1) / nblk);
   ns = std::min(ns, 4 * 148);
   ns = (int)std::max(1LL, std::min<long long>(ns, (len + 4 * KC - 1) / (4 * KC)));
   long long rps = (len + ns - 1) / ns;

@@ -31,6 +31,12 @@ struct PassArgsH {
   int z0 = 0, nz = 0;  // x/y passes: restrict to z-planes [z0, z0+nz) (nz = 0: all)
 };
 
+// Persistent-grid share: the block-update and Gram kernels size their grids to this fraction of
+// (148 SMs x resident CTAs per SM), so that kernels of concurrent k-point solves (other streams)
+// can co-reside (process-wide tuning knob, pc_set_option "grid_frac"; default 1).
+void set_grid_frac(double f);
+int grid_cap(int ctas_per_sm);
+
 // FFT passes ------------------------------------------------------------------------------
 // kind: 0 plain (C=1), 1 inverse-z with K_A^H prologue (C=3), 2 forward-z with K_A+gamma K_B (C=3)
 // in/out/xh: per-column pointers (xh only for kind 2: the apply's input x_hat), ncols <= PC_MAXCOLS.
@@ -108,6 +114,25 @@ int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C,
                       const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
                       int deflate0, double* partial, int max_grid, cudaStream_t st);
+
+// Same contract as launch_update_all with the row tiles streamed by TMA tensor copies (update_tmap.cu).
+// The basis is given per block k (0: X, 1: W, 2: P) as a column range of one LOBPCG slot: s[k] / as[k]
+// = column 0 of the S / AS slot (slot_cols[k] columns, column stride ld complex), box columns
+// [c0[k], c0[k] + nc[k]) (nc[k] <= 32; 0 = block absent), crow[k][j] = row of C for box column j
+// (-1: not in the basis).  Returns the grid, or -1 if the tensor maps cannot be encoded.
+struct UtBlocks {
+  const cplx* s[3];
+  const cplx* as[3];
+  int slot_cols[3];
+  long long ld;
+  int c0[3], nc[3];
+  signed char crow[3][32];
+};
+bool update_tmap_supported(int n, int b);
+int launch_update_tmap(const UtBlocks& blk, const cplx* C, int ldc, int r, const MutColPtrs& Y1s,
+                       const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a, const MutColPtrs& W,
+                       const double* lam, int n, const cplx* kt, double gamma, double thr, int deflate0,
+                       double* partial, int max_grid, cudaStream_t st);
 
 // Update + residual + K_P^{-1} + the next iteration's Gram blocks in one pass (update_gram.cu):
 // S = [X W P] (p columns, X first: split = b), outputs X', AX' (b columns), P', AP', W' (nw columns,

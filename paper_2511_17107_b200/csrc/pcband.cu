@@ -150,6 +150,7 @@ struct pc_ctx {
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
+  int update_tmap = 1;         // 1: update kernel with TMA tensor-copy row tiles (update_tmap.cu); 0: cp.async tiles
   int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
   int gram_derive = 0;         // 1: P blocks of the Gram from the previous Gram and Ritz coefficients (see solve_k; unstable)
   double derive_tau = 1e5;     // ... unless their cancellation factor exceeds this (then from the vectors)
@@ -457,8 +458,10 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "derive_tau") c->derive_tau = v;
   else if (k == "xdev_tol") c->xdev_tol = v;
   else if (k == "update_stream") c->update_stream = (int)v;
+  else if (k == "update_tmap") c->update_tmap = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
+  else if (k == "grid_frac") set_grid_frac(v);
   else if (k == "update_tma") set_update_tma((int)v);
   else if (k == "update_compact") set_update_compact((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
@@ -821,6 +824,114 @@ extern "C" int pc_debug_heevj(const double* A_host, int n, double* w_host, doubl
   cudaFree(dV);
   cudaFree(dw);
   cudaFree(di);
+  return PC_OK;
+}
+
+// Kernel timing entry for the LOBPCG block kernels on random data (tools/bench_block.py): the shapes
+// of one iteration with b X columns, na W columns and nP P columns on this context's grid.
+// which = 0: fused update (+ residual, K_P^{-1}); 1: Gram S^H [W P AW AP] (+ assembly); 2: Gram
+// S^H [W AW].  ms = mean milliseconds per launch group over reps (CUDA events on the context stream).
+extern "C" int pc_bench_block(pc_ctx* c, int which, int b, int na, int nP, int reps, double* ms) {
+  if (!c || !ms || b < 1 || na < 0 || nP < 0 || nP > na || na > b || reps < 1)
+    return set_err(PC_EINVAL, "pc_bench_block: bad arguments");
+  const int p = b + na + nP;
+  if (3 * b > 80 || p > 80) return set_err(PC_EINVAL, "pc_bench_block: p <= 80");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = c->stream;
+  const long long len = c->len;
+  {
+    const double k[3] = {0.5, 0.3, 0.2};
+    set_k(c, k, st);
+  }
+  CHK(c->lob.ensure(10 * (size_t)b * len * sizeof(cplx)));
+  cplx* base = c->lob.as<cplx>();
+  auto col = [&](int slot, int j) { return base + ((size_t)slot * b + j) * len; };
+  MutColPtrs all;
+  for (int j = 0; j < 8 && j * b < PC_MAXCOLS; j++) {
+    int nc = std::min(b, PC_MAXCOLS - j * b);
+    for (int t = 0; t < nc; t++) all.p[t] = col(j, t);
+    launch_randn(all, nc, len, 1234 + j, 0, 1.0, st);
+  }
+  const int rg = resid_grid(c->n);
+  const size_t nG = (size_t)p * 2 * p;
+  CHK(c->small.ensure((2 * nG + (size_t)p * b) * sizeof(cplx) + (size_t)(b + rg * b * 2) * sizeof(double) + 64));
+  CHK(c->gpart.ensure(gram_partial_bytes(p, 2 * p)));
+  cplx* dG = c->small.as<cplx>();
+  cplx* dGp = dG + nG;
+  cplx* dC = dGp + nG;
+  double* dLam = reinterpret_cast<double*>(dC + (size_t)p * b);
+  double* dPart = dLam + b;
+  {
+    MutColPtrs cm;
+    cm.p[0] = dC;
+    launch_randn(cm, 1, (long long)p * b, 99, 0, 0.1, st);
+    cudaMemsetAsync(dLam, 0, b * sizeof(double), st);
+  }
+  // S = [X(slot 0) W(slot 8) P(slot 4)], AS = [AX(1) AW(9) AP(5)]; outputs X' 2, AX' 3, P' 6, AP' 7, W 8
+  ColPtrs S, AS;
+  for (int j = 0; j < b; j++) { S.p[j] = col(0, j); AS.p[j] = col(1, j); }
+  for (int j = 0; j < na; j++) { S.p[b + j] = col(8, j); AS.p[b + j] = col(9, j); }
+  for (int j = 0; j < nP; j++) { S.p[b + na + j] = col(4, j); AS.p[b + na + j] = col(5, j); }
+  MutColPtrs Y1, Y2, Y1a, Y2a, W;
+  for (int j = 0; j < b; j++) {
+    Y2.p[j] = col(2, j);
+    Y2a.p[j] = col(3, j);
+    Y1.p[j] = j < na ? col(6, j) : nullptr;
+    Y1a.p[j] = j < na ? col(7, j) : nullptr;
+    W.p[j] = j < na ? col(8, j) : nullptr;
+  }
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  double tot = 0.0;
+  for (int r = -1; r < reps; r++) {  // r = -1: warm-up
+    cudaEventRecord(e0, st);
+    if (which == 0) {
+      // W is read (S) and overwritten tile by tile, as in pc_bands
+      const int g = launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                      1.0, 0.0, 0, dPart, rg, st);
+      launch_reduce_partial(dPart, g, b, dLam + 0 * b, st);
+    } else if (which == 3) {
+      UtBlocks blk;
+      memset(&blk, 0, sizeof(blk));
+      blk.ld = len;
+      const int slotS[3] = {0, 8, 4}, slotA[3] = {1, 9, 5}, cnt[3] = {b, na, nP}, rowoff[3] = {0, b, b + na};
+      for (int kb = 0; kb < 3; kb++) {
+        if (!cnt[kb]) continue;
+        blk.s[kb] = col(slotS[kb], 0);
+        blk.as[kb] = col(slotA[kb], 0);
+        blk.slot_cols[kb] = b;
+        blk.c0[kb] = 0;
+        blk.nc[kb] = cnt[kb];
+        for (int j = 0; j < 32; j++) blk.crow[kb][j] = j < cnt[kb] ? (signed char)(rowoff[kb] + j) : -1;
+      }
+      const int g = launch_update_tmap(blk, dC, p, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab, 1.0, 0.0, 0,
+                                       dPart, rg, st);
+      if (g < 0) return set_err(PC_ECUDA, "pc_bench_block: tensor map encoding failed");
+      launch_reduce_partial(dPart, g, b, dLam + 0 * b, st);
+    } else if (which == 1) {
+      ColPtrs T;
+      const int cw = na + nP;
+      for (int t = 0; t < cw; t++) T.p[t] = S.p[b + t];
+      for (int t = 0; t < cw; t++) T.p[cw + t] = AS.p[b + t];
+      launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st);
+      launch_gram_assemble(dGp, dLam, b, cw, dG, st);
+    } else {
+      ColPtrs T;
+      for (int t = 0; t < na; t++) T.p[t] = S.p[b + t];
+      for (int t = 0; t < na; t++) T.p[na + t] = AS.p[b + t];
+      launch_gram(S, p, T, 2 * na, len, dGp, c->gpart.as<cplx>(), st);
+    }
+    cudaEventRecord(e1, st);
+    CU(cudaEventSynchronize(e1));
+    float m = 0.f;
+    cudaEventElapsedTime(&m, e0, e1);
+    if (r >= 0) tot += m;
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  CU(cudaGetLastError());
+  *ms = tot / reps;
   return PC_OK;
 }
 
@@ -1247,11 +1358,35 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
           if (!wr[j]) W.p[j] = nullptr;
           hasW[j] = wr[j];
         }
-        const int g = c->update_stream
-                          ? launch_update_stream(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
-                                                 c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st)
-                          : launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
-                                              c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+        int g = -1;
+        if (c->update_tmap && update_tmap_supported(c->n, b)) {
+          // basis blocks as column ranges of the X, W and P slots (holes = soft-locked columns)
+          UtBlocks blk;
+          memset(&blk, 0, sizeof(blk));
+          blk.ld = len;
+          const int slotS[3] = {sX, WW, sP}, slotA[3] = {sAX, AWW, sAP};
+          const std::vector<int>* lists[3] = {&all, &act, &actP};
+          const int rowoff[3] = {0, b, b + na};
+          for (int kb = 0; kb < 3; kb++) {
+            const std::vector<int>& L = *lists[kb];
+            if (L.empty() || (kb == 2 && !haveP)) continue;
+            blk.s[kb] = col(slotS[kb], 0);
+            blk.as[kb] = col(slotA[kb], 0);
+            blk.slot_cols[kb] = b;
+            blk.c0[kb] = L.front();
+            blk.nc[kb] = L.back() - L.front() + 1;
+            for (int j = 0; j < 32; j++) blk.crow[kb][j] = -1;
+            for (size_t t = 0; t < L.size(); t++) blk.crow[kb][L[t] - L.front()] = (signed char)(rowoff[kb] + t);
+          }
+          g = launch_update_tmap(blk, dC, p, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab, c->cur_gamma,
+                                 c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+        }
+        if (g < 0)
+          g = c->update_stream
+                  ? launch_update_stream(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                         c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st)
+                  : launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
+                                      c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
         resid_ready = true;
       } else {

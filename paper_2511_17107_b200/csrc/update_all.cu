@@ -15,10 +15,15 @@
 #include "kp.cuh"
 #include "tma.cuh"
 
-constexpr int UA_SEG = 16;               // modes per tile
+#ifndef PC_UA_SEG
+#define PC_UA_SEG 16
+#endif
+constexpr int UA_SEG = PC_UA_SEG;        // modes per tile (multiple of 8)
+constexpr int UA_RG = UA_SEG / 8;        // 8-mode row groups per component
 constexpr int UA_ROWS = 3 * UA_SEG;      // rows per tile (3 components)
 constexpr int UA_RP = UA_ROWS + 2;       // smem row pitch (complex), 2 mod 8
-constexpr int UA_THREADS = 128;          // warp w: modes [8 (w & 1), +8), n-tiles {w >> 1, +2, ...}
+constexpr int UA_WARPS = 2 * UA_RG;      // warp w: modes [8 (w % UA_RG), +8), n-tiles {w / UA_RG, +2, ...}
+constexpr int UA_THREADS = 32 * UA_WARPS;
 
 HD int ua_pitch4mod8(int p) {
   int x = p;
@@ -32,13 +37,13 @@ HD int ua_pitch4mod8(int p) {
 // unpadded tile pitch of 48 rows with an XOR row swizzle, 55 KB instead of 67 KB of shared memory per
 // CTA: 4 CTAs per SM instead of 3.
 template <int NT, bool TMA, bool CPT>
-__global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 4 : 1) update_all_kernel(
+__global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) update_all_kernel(
     ColPtrs S, ColPtrs AS, int p, const cplx* __restrict__ C, int ldc, int r, int split, MutColPtrs Y1s,
     MutColPtrs Y2s, MutColPtrs Y1a, MutColPtrs Y2a, MutColPtrs Wout, const double* __restrict__ lam, int n,
     const cplx* __restrict__ kt, double gamma, double thr, int deflate0, double* partial) {
   constexpr int NTW = (NT + 1) / 2;
   extern __shared__ __align__(16) double uasm[];
-  __shared__ double red[4][NTW][4][2][2];
+  __shared__ double red[UA_WARPS][NTW][4][2][2];
   __shared__ __align__(8) unsigned long long mbar[2];
   const int n3 = n * n * n;
   const int pe = (p + 3) & ~3;
@@ -51,7 +56,7 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 4 : 1) update_all_kern
   cplx* Buf = reinterpret_cast<cplx*>(uasm);  // [2][pe][RP]: buffer 0 = S tiles, 1 = AS tiles
   cplx* Cs = Buf + 2 * pe * RP;               // [NT*8][PS] (not with CPT)
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int rg = warp & 1, ng = warp >> 1;
+  const int rg = warp % UA_RG, ng = warp / UA_RG;
 
   for (int e = tid; e < NT * 8 * pe; e += UA_THREADS) {
     int c = e / pe, m = e % pe;
@@ -136,6 +141,9 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 4 : 1) update_all_kern
           if (!in) cv = mk(0, 0);
         }
         const double cs = cv.x + cv.y;
+#ifdef PC_UA_NOMMA  // timing experiment: memory traffic only (results wrong)
+        if (cs != 12345.0) continue;
+#endif
 #pragma unroll
         for (int s = 0; s < 3; s++) {
           dmma(p1[s][i][0], p1[s][i][1], a[s].x, cv.x);
@@ -267,9 +275,9 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 4 : 1) update_all_kern
     const int nt = c / 8, i = nt >> 1, g = nt & 1;
     const int ln = (c % 8) / 2, e = c % 2;
     double a = 0, b = 0;
-    for (int q = 0; q < 2; q++) {  // the two row-group warps of n-tile group g, fixed order
-      a += red[2 * g + q][i][ln][e][0];
-      b += red[2 * g + q][i][ln][e][1];
+    for (int q = 0; q < UA_RG; q++) {  // the row-group warps of n-tile group g, fixed order
+      a += red[UA_RG * g + q][i][ln][e][0];
+      b += red[UA_RG * g + q][i][ln][e][1];
     }
     partial[((long long)c * gridDim.x + blockIdx.x) * 2 + 0] = a;
     partial[((long long)c * gridDim.x + blockIdx.x) * 2 + 1] = b;
@@ -300,7 +308,7 @@ static int run_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx
   occ = std::max(1, std::min(8, occ));
   const long long n3 = (long long)n * n * n;
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
-  const int grid = (int)std::min<long long>(std::min<long long>(ntiles, 148LL * occ), max_grid);
+  const int grid = (int)std::min<long long>(std::min<long long>(ntiles, (long long)grid_cap(occ)), max_grid);
   kern<<<grid, UA_THREADS, smem, st>>>(S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr,
                                        deflate0, partial);
   return grid;
