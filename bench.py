@@ -448,7 +448,9 @@ def main():
         e2e_job([kidx(0)])
         torch.cuda.synchronize()
         t0 = time.perf_counter()
-        eidx = [kidx(s) for s in range(args.e2e_steps)]
+        # the same k-points as the timed device steps (when e2e_steps == steps), so E and value differ only
+        # by what the end-to-end path adds (uploads, context setup, host round trips)
+        eidx = [kidx(s) for s in range(nwarm, nwarm + args.e2e_steps)]
         e_it = [int(v) for v in e2e_job(eidx)[2]]
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
@@ -460,7 +462,7 @@ def main():
         h2d = (nctx * (W.n ** 3 + 16 * W.n)) / args.e2e_steps + 24
         d2h = int(np.mean(e_it)) * (2 * b * 8 + 8) + b * 8
         e2e = {"value": world * args.e2e_steps / float(tt.item()), "unit": "k-points/s",
-               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "iters": e_it,
                "note": f"one job of {args.e2e_steps} k-points per rank: pc_create x {nctx} from pinned host masks "
                        "(upload included) + bands.solve_concurrent with host k-points and host omega^2/Res "
                        "outputs + pc_destroy, wall clock"}

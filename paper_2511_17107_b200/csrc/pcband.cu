@@ -5,7 +5,9 @@
 // (P:523-529), preconditioned by K_P^{-1}, until Res_j <= tol for the nev smallest pairs
 // (P:1059-1064).  Everything on the data path runs in this library's kernels; the host only decides
 // which columns are still active (one D2H of 2b doubles per iteration) and sequences launches.
+#include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <map>
@@ -167,7 +169,7 @@ struct pc_ctx {
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
-  DevBuf lob, small, gpart, ugbuf;
+  DevBuf lob, small, gpart, ugbuf, cbuf;
   double* h_pinned = nullptr;
   cudaStream_t stream = nullptr;
   // profiling
@@ -366,7 +368,13 @@ extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double ep
       if (masks[f * c->n3 + i]) b |= (uint8_t)(1u << f);
     packed[i] = b;
   }
-  if (cudaMalloc(&c->d_mask, c->n3) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: mask alloc");
+  // twiddles, symbol table and mask in one cached block (no cudaMalloc / cudaFree per context: a
+  // cudaFree can stall for hundreds of ms while other contexts run)
+  if (c->cbuf.ensure((size_t)10 * n * sizeof(cplx) + (size_t)c->n3 + 256) != PC_OK)
+    return fail(PC_ENOMEM, "pc_create: table alloc");
+  c->d_tw = c->cbuf.as<cplx>();
+  c->d_ktab = c->d_tw + n;
+  c->d_mask = reinterpret_cast<uint8_t*>(c->d_ktab + 9 * n);
   if (cudaMemcpy(c->d_mask, packed.data(), c->n3, cudaMemcpyHostToDevice) != cudaSuccess)
     return fail(PC_ECUDA, "pc_create: mask upload");
   // twiddles exp(-2 pi i j / N) in long double, rounded once
@@ -381,9 +389,7 @@ extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double ep
       tw[j] = mk(cs[qd][0], cs[qd][1]);
     }
   }
-  if (cudaMalloc(&c->d_tw, n * sizeof(cplx)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: twiddle alloc");
   cudaMemcpy(c->d_tw, tw.data(), n * sizeof(cplx), cudaMemcpyHostToDevice);
-  if (cudaMalloc(&c->d_ktab, 9 * n * sizeof(cplx)) != cudaSuccess) return fail(PC_ENOMEM, "pc_create: ktab alloc");
   if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess)
     return fail(PC_ECUDA, "pc_create: stream");
   if (cudaMallocHost(&c->h_pinned, PIN_DOUBLES * sizeof(double)) != cudaSuccess)
@@ -394,13 +400,16 @@ extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double ep
 
 extern "C" void pc_destroy(pc_ctx* c) {
   if (!c) return;
+  static const bool trace = getenv("PCBAND_TRACE") != nullptr;
+  auto now = [] { return std::chrono::steady_clock::now(); };
+  auto t0 = now();
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
   prof_flush(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
-  if (c->d_mask) cudaFree(c->d_mask);
-  if (c->d_tw) cudaFree(c->d_tw);
-  if (c->d_ktab) cudaFree(c->d_ktab);
+  auto t1 = now();
+  c->cbuf.release();
+  auto t2 = now();
   c->ws.release();
   c->kxws.release();
   c->ugbuf.release();
@@ -408,8 +417,16 @@ extern "C" void pc_destroy(pc_ctx* c) {
   c->small.release();
   c->gpart.release();
   c->pwbuf.release();
+  auto t3 = now();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  auto t4 = now();
   if (c->stream) cudaStreamDestroy(c->stream);
+  auto t5 = now();
+  if (trace) {
+    auto ms = [](auto a, auto b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+    fprintf(stderr, "[pcband] destroy: sync %.1f ms, tables %.1f, cache %.1f, freehost %.1f, stream %.1f\n",
+            ms(t0, t1), ms(t1, t2), ms(t2, t3), ms(t3, t4), ms(t4, t5));
+  }
   delete c;
 }
 
