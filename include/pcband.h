@@ -192,6 +192,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  update launches and a separate residual pass
  *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)
  *   "update_warps" 4 (default), 8 or 16 warps per block-update CTA (process-wide tuning knob)
+ *   "gram_tmap"    1: Gram S^H [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu, S and T
+ *                  share one shared-memory buffer; measured slower); 0 (default): cp.async chunks (gram.cu)
  *   "update_tmap"  1 (default): block-update kernel with TMA tensor-copy row tiles in a 2-stage
  *                  ring (update_tmap.cu); 0: per-thread cp.async tiles (update_all.cu)
  *   "gram_ks"      2 (default) or 1 warp groups splitting each Gram row chunk (process-wide knob)
@@ -252,8 +254,8 @@ int pc_history(const pc_ctx *ctx, double *out, int cap, int *block);
  * pc_bench_block — timing entry for the LOBPCG block kernels on random device data
  * in this context's workspace (overwrites any LOBPCG state): the shapes of one iteration with b X
  * columns, na W columns and nP P columns (nP <= na <= b, b + na + nP <= 80, 3b <= 80).  which = 0:
- * fused block update + residual + K_P^{-1} (one launch group as in pc_bands); 1: Gram
- * S^H [W P AW AP] + assembly; 2: Gram S^H [W AW].  *ms = mean CUDA-event milliseconds per launch
+ * fused block update + residual + K_P^{-1} (one launch group as in pc_bands; 3: the TMA variant);
+ * 1: Gram S^H [W P AW AP] + assembly (4: the TMA variant); 2: Gram S^H [W AW].  *ms = mean CUDA-event milliseconds per launch
  * group over reps (after one warm-up), on the context's stream.  Synchronous.
  */
 int pc_bench_block(pc_ctx *ctx, int which, int b, int na, int nP, int reps, double *ms);

@@ -91,6 +91,22 @@ int launch_gram_derive(const cplx* G0, int p0, const cplx* C0, const int* actP, 
 // strict lower triangles are skipped (left unwritten in G; launch_gram_assemble mirrors them).
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                  cudaStream_t st, int hb = -1, int hc = 0);
+// Gp = S^H T for S = [X W P], T = [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu).  Block k
+// (0 X, 1 W, 2 P, 3 AW, 4 AP) = box columns [c0[k], c0[k] + nc[k]) of a slot (base[k] = its column 0,
+// slot_cols[k] columns, stride ld); lidx[k][j] (k < 3) / tidx[k][j] (k >= 1) = row of Gp / column of
+// Gp of box column j (-1: not in the basis).  Gp is p x q column-major (p, q from the maps), written
+// by a fixed-order reduction of the CTA partials in `partial` (>= gram_tmap_partial_bytes()).
+// Returns -1 (nothing launched) if the shape is not supported (S > 40 or T > 40 columns).
+struct GtBlocks {
+  const cplx* base[5];
+  int slot_cols[5];
+  long long ld;
+  int c0[5], nc[5];
+  signed char lidx[5][32], tidx[5][32];
+};
+size_t gram_tmap_partial_bytes();
+int launch_gram_tmap(const GtBlocks& blk, long long len, cplx* G, cplx* partial, cudaStream_t st);
+
 // Block update (r <= 32 output columns, C column-major ld = ldc):
 //   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr; columns with Y1->p[c] == nullptr skipped)
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])

@@ -152,6 +152,7 @@ struct pc_ctx {
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
+  int gram_tmap = 0;           // 1: Gram S^H [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu; slower)
   int update_tmap = 1;         // 1: update kernel with TMA tensor-copy row tiles (update_tmap.cu); 0: cp.async tiles
   int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
   int gram_derive = 0;         // 1: P blocks of the Gram from the previous Gram and Ritz coefficients (see solve_k; unstable)
@@ -476,6 +477,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "xdev_tol") c->xdev_tol = v;
   else if (k == "update_stream") c->update_stream = (int)v;
   else if (k == "update_tmap") c->update_tmap = (int)v;
+  else if (k == "gram_tmap") c->gram_tmap = (int)v;
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "grid_frac") set_grid_frac(v);
@@ -926,6 +928,26 @@ extern "C" int pc_bench_block(pc_ctx* c, int which, int b, int na, int nP, int r
                                        dPart, rg, st);
       if (g < 0) return set_err(PC_ECUDA, "pc_bench_block: tensor map encoding failed");
       launch_reduce_partial(dPart, g, b, dLam + 0 * b, st);
+    } else if (which == 4) {
+      GtBlocks gb;
+      memset(&gb, -1, sizeof(gb));
+      gb.ld = len;
+      const int cw = na + nP;
+      const int slots[5] = {0, 8, 4, 9, 5}, cnt[5] = {b, na, nP, na, nP};
+      const int lofs[5] = {0, b, b + na, -1, -1}, tofs[5] = {-1, 0, na, cw, cw + na};
+      for (int kb = 0; kb < 5; kb++) {
+        gb.base[kb] = col(slots[kb], 0);
+        gb.slot_cols[kb] = b;
+        gb.c0[kb] = 0;
+        gb.nc[kb] = cnt[kb];
+        for (int j = 0; j < cnt[kb]; j++) {
+          gb.lidx[kb][j] = (signed char)(lofs[kb] >= 0 ? lofs[kb] + j : -1);
+          gb.tidx[kb][j] = (signed char)(tofs[kb] >= 0 ? tofs[kb] + j : -1);
+        }
+      }
+      if (launch_gram_tmap(gb, len, dGp, c->gpart.as<cplx>(), st) != 0)
+        return set_err(PC_EINVAL, "pc_bench_block: shape not supported by gram_tmap");
+      launch_gram_assemble(dGp, dLam, b, cw, dG, st);
     } else if (which == 1) {
       ColPtrs T;
       const int cw = na + nP;
@@ -1301,7 +1323,33 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         ccols(AWW, act, T, cw);
         if (haveP) ccols(sAP, actP, T, cw + na);
         Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * cw, 16.0 * len * (p + cw));
-        launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st, c->gram_herm ? b : -1, cw);
+        int gt = -1;
+        if (c->gram_tmap && !c->gram_herm) {
+          // the five blocks as column ranges of their slots (holes = soft-locked columns)
+          GtBlocks gb;
+          memset(&gb, -1, sizeof(gb));
+          gb.ld = len;
+          const int slots[5] = {sX, WW, sP, AWW, sAP};
+          const std::vector<int>* lists[5] = {&all, &act, &actP, &act, &actP};
+          const int lofs[5] = {0, b, b + na, -1, -1}, tofs[5] = {-1, 0, na, cw, cw + na};
+          for (int kb = 0; kb < 5; kb++) {
+            const std::vector<int>& L = *lists[kb];
+            gb.base[kb] = col(slots[kb], 0);
+            gb.slot_cols[kb] = b;
+            gb.c0[kb] = 0;
+            gb.nc[kb] = 0;
+            if (L.empty() || ((kb == 2 || kb == 4) && !haveP)) continue;
+            gb.c0[kb] = L.front();
+            gb.nc[kb] = L.back() - L.front() + 1;
+            for (size_t t = 0; t < L.size(); t++) {
+              const int j = L[t] - L.front();
+              gb.lidx[kb][j] = (signed char)(lofs[kb] >= 0 ? lofs[kb] + (int)t : -1);
+              gb.tidx[kb][j] = (signed char)(tofs[kb] >= 0 ? tofs[kb] + (int)t : -1);
+            }
+          }
+          gt = launch_gram_tmap(gb, len, dGp, c->gpart.as<cplx>(), st);
+        }
+        if (gt < 0) launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st, c->gram_herm ? b : -1, cw);
         launch_gram_assemble(dGp, dLam, b, cw, dG, st);
       }
       rank = rr(p);

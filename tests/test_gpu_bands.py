@@ -77,12 +77,14 @@ def test_homogeneous_n8_golden(api):
 ])
 @pytest.mark.parametrize("tmap", [0, 1])
 def test_bands_match_dense_oracle(api, lat, n, k, eps, geo, tmap):
-    """Both block-update kernels (cp.async tiles / TMA tensor copies; n = 6 has a ragged last tile)."""
+    """Both block-update and Gram kernel families (cp.async tiles / TMA tensor copies; n = 6 has a
+    ragged last tile)."""
     A = synth.lattice(lat)
     e = {"pc": synth.eps_pseudochiral(), "sdd": synth.eps_sdd(), "iso": synth.eps_isotropic(13.0)}[eps]
     masks = synth.make_masks(geo, A, n, seed=31)
     ctx = api.pc_create(A, n, e, masks)
     api.pc_set_option(ctx, "update_tmap", tmap)
+    api.pc_set_option(ctx, "gram_tmap", tmap)
     r = api.pc_bands(ctx, [k], nev=10, tol=TOL)
     assert r["status"][0] == 0
     op = O.PenalizedOperator(n, np.array(k), A, e, masks)
@@ -219,7 +221,7 @@ def test_bands_warm_start_path_continuation(api):
                                   {"update_tma": 1}, {"gram_refresh": 1}, {"gram_herm": 1},
                                   {"update_compact": 1}, {"trim_locked": 0}, {"sticky_lock": 1},
                                   {"update_stream": 1}, {"gram_derive": 1}, {"update_tmap": 1},
-                                  {"update_tmap": 0}])
+                                  {"update_tmap": 0}, {"gram_tmap": 0}, {"gram_tmap": 1, "sticky_lock": 1}])
 def test_bands_option_variants(api, opts):
     """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
     tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""

@@ -35,7 +35,7 @@ for w in a.which:
     ms = api.pc_bench_block(ctx, w, a.b, a.na, a.np, a.reps)
     if w in (0, 3):
         cols = 2 * p + 2 * a.b + 3 * a.na
-    elif w == 1:
+    elif w in (1, 4):
         cols = p + 2 * (a.na + a.np)
     else:
         cols = p + a.na
