@@ -184,7 +184,7 @@ def workload_config(W, args):
     return {"workload": f"{W.name}: {W.lattice.upper()} lattice, {W.geometry} inclusion, eps1={W.eps} "
                         f"(pseudochiral eps_lat=13 beta=0.875, PAPER.md:1083-1093), n={W.n}, {W.nev} bands, "
                         f"tol={args.tol:g}, k-path {len(W.kpoints())} points",
-            "n": W.n, "nev": W.nev, "block": W.nev + 5, "tol": args.tol, "lattice": W.lattice,
+            "n": W.n, "nev": W.nev, "block": W.nev + (args.guard if args.guard is not None else 6), "tol": args.tol, "lattice": W.lattice,
             "geometry": W.geometry, "eps_mode": "crossdof",
             "l2": "no flush: per-k working set ~15 GB >> 126 MB L2",
             "start": ("warm: each context solves a contiguous k stretch, k_i started from k_(i-1)'s Ritz block "
@@ -457,7 +457,7 @@ def main():
         tt = torch.tensor([te], dtype=torch.float64, device=cdev)
         if world > 1:
             dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        b = W.nev + (args.guard if args.guard is not None else 5)
+        b = W.nev + (args.guard if args.guard is not None else 6)
         # per context: packed indicator masks (1 B/point) + twiddles and symbol tables; per k: 24 B k-point
         h2d = (nctx * (W.n ** 3 + 16 * W.n)) / args.e2e_steps + 24
         d2h = int(np.mean(e_it)) * (2 * b * 8 + 8) + b * 8

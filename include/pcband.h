@@ -158,7 +158,7 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
 
 /*
  * pc_set_option — tuning knobs (return PC_EINVAL for unknown keys):
- *   "guard"        extra LOBPCG block columns beyond nev (default 5)
+ *   "guard"        extra LOBPCG block columns beyond nev (default 6)
  *   "apply_chunk"  max columns per batched apply (default 0 = all at once)
  *   "profile"      1: time every kernel class with CUDA events (read with pc_stats), 0: off
  *   "drop_tol"     Rayleigh-Ritz rank threshold on the scaled Gram eigenvalues (default 1e-12)

@@ -141,7 +141,7 @@ struct pc_ctx {
   DevBuf ws;          // apply workspace
   DevBuf kxws;        // apply workspace: gamma (kappa . xhat), N^3 per column (first pass -> last pass)
   int apply_chunk = 0;
-  int guard = 5;
+  int guard = 6;  // block b = nev + guard (reading R14; measured optimum of the current kernels)
   double drop_tol = 1e-12;
   long long kindex_offset = 0;  // global index of kpts[0] (seeds independent of sharding)
   int verbose = 0;
