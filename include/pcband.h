@@ -197,6 +197,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "update_tmap"  1 (default): block-update kernel with TMA tensor-copy row tiles in a 2-stage
  *                  ring (update_tmap.cu); 0: per-thread cp.async tiles (update_all.cu)
  *   "gram_ks"      2 (default) or 1 warp groups splitting each Gram row chunk (process-wide knob)
+ *   "jacobi_tol"   rotation threshold of the Rayleigh-Ritz Jacobi sweeps, |a_pq| <= tol sqrt(|a_pp a_qq|)
+ *                  (process-wide; default 1e-16)
  *   "grid_frac"    (0, 1]: persistent block-update and Gram grids cover this fraction of the GPU's
  *                  resident-CTA slots, leaving room for concurrent solves (process-wide; default 1)
  */

@@ -173,5 +173,6 @@ void launch_ug_assemble(const cplx* red, int b, int nw, const int* act, int na, 
 // info[1] = sweeps of the last Jacobi.  Uses scratch (>= 4 p^2 complex).
 void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* lambda, int* info, cplx* scratch,
                cudaStream_t st);
+void set_jacobi_tol(double t);  // tuning knob: Jacobi rotation threshold of the Rayleigh-Ritz step
 // Dense Hermitian eigensolver (one-CTA Jacobi) for tests: A (n x n, ld n) -> w (n, ascending), V (n x n).
 void launch_heevj(const cplx* A, int n, double* w, cplx* V, int* info, cudaStream_t st);

@@ -481,6 +481,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "update_warps") set_update_warps((int)v);
   else if (k == "gram_ks") set_gram_ks((int)v);
   else if (k == "grid_frac") set_grid_frac(v);
+  else if (k == "jacobi_tol") set_jacobi_tol(v);
   else if (k == "update_tma") set_update_tma((int)v);
   else if (k == "update_compact") set_update_compact((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;

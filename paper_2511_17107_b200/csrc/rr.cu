@@ -30,7 +30,7 @@ DEV void tpair(int r, int i, int m, int& P, int& Q) {
 }
 
 // A, V column-major with leading dimension ld (= np).  A Hermitian n x n zero-padded to np (even).
-DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps) {
+DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps, double rel_tol = 1e-16) {
   const int tid = threadIdx.x;
   const int h = np / 2;
   int sweep = 0;
@@ -47,7 +47,7 @@ DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_
           cplx apq = A[P + Q * ld];
           double mag = hypot(apq.x, apq.y);
           double app = A[P + P * ld].x, aqq = A[Q + Q * ld].x;
-          if (mag > 1e-300 && mag > 1e-16 * sqrt(fabs(app * aqq))) {
+          if (mag > 1e-300 && mag > rel_tol * sqrt(fabs(app * aqq))) {
             double z = (aqq - app) / (2.0 * mag);
             double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
             c = 1.0 / sqrt(1.0 + t * t);
@@ -137,7 +137,8 @@ DEV bool cholesky_smem(cplx* A, int n, int ld, double tau, int* flag) {
 }
 
 __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__ G, int p, int nb, double drop_tol,
-                                                        cplx* Cout, double* lam, int* info, cplx* scratch) {
+                                                        cplx* Cout, double* lam, int* info, cplx* scratch,
+                                                        double jtol) {
   extern __shared__ __align__(16) unsigned char rsm[];
   const int np = (p + 1) & ~1, ld = np;
   cplx* A = reinterpret_cast<cplx*>(rsm);
@@ -276,7 +277,7 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
     __syncthreads();
   }
   // 3. eig of H (r x r, ld rp)
-  int sw = jacobi_smem(A, V, r, rp, rp, js, 40);
+  int sw = jacobi_smem(A, V, r, rp, rp, js, 40, jtol);
   for (int i = tid; i < r; i += blockDim.x) sig[i] = A[i + i * rp].x;
   __syncthreads();
   rank_sort(sig, r, order);
@@ -320,6 +321,11 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   }
 }
 
+// Rotation threshold of the Rayleigh-Ritz Jacobi: |a_pq| <= tol sqrt(|a_pp a_qq|) counts as zero (the
+// eigenvalues it leaves out are O(tol^2) relative; eigenvectors O(tol)).  Process-wide tuning knob.
+static double g_jacobi_tol = 1e-16;
+void set_jacobi_tol(double t) { g_jacobi_tol = (t > 0.0 && t < 1e-6) ? t : 1e-16; }
+
 void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* lambda, int* info, cplx* scratch,
                cudaStream_t st) {
   const int np = (p + 1) & ~1;
@@ -330,7 +336,7 @@ void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* l
                          (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
     attr = true;
   }
-  rr_kernel<<<1, RR_THREADS, smem, st>>>(G, p, nb, drop_tol, C, lambda, info, scratch);
+  rr_kernel<<<1, RR_THREADS, smem, st>>>(G, p, nb, drop_tol, C, lambda, info, scratch, g_jacobi_tol);
 }
 
 // Standalone Hermitian eigensolver (tests): w ascending, V columns in the same order.

@@ -19,9 +19,9 @@
 //   dim3: columns (ld*16 B).  Box (16, 2, 3, nc) = 16 modes x 3 components x nc columns, landing in
 // shared memory as [column][component][half][128 B] with the 128-B swizzle (16-B chunk j of 128-B row
 // r at chunk j ^ (r & 7)), which makes the DMMA A-fragment loads (8 modes x 4 columns per quarter
-// warp) conflict-free without padding.  A block starts at a multiple of 4 columns (3072 B, a multiple
-// of the 1024-B swizzle atom); columns of a box that are not in the basis (soft-locked columns
-// between active ones) and the padding columns get zero rows of C.
+// warp) conflict-free without padding.  A block starts at an even column (see PC_UT_ALIGN); columns of
+// a box that are not in the basis (soft-locked columns between active ones) and the padding columns
+// get zero rows of C.
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include "kernels.h"
@@ -38,6 +38,12 @@ constexpr int UT_THREADS = 128;         // warp w: modes [8 (w & 1), +8), n-tile
 #define PC_UT_MINB 3
 #endif
 constexpr int UT_STAGES = PC_UT_STAGES;
+#ifndef PC_UT_ALIGN
+// block starts in columns: the tensor copies swizzle on absolute shared-memory address bits, so a box
+// may start inside a 1024-B swizzle atom (parity-tested with 1, 2 and 4); even starts (1536 B) keep the
+// basis at 36 stage columns for b = 15, 16 (40 with 4) and measured fastest (2.34 vs 2.50 ms)
+#define PC_UT_ALIGN 2
+#endif
 #ifndef PC_UT_UNROLL
 #define PC_UT_UNROLL 4
 #endif
@@ -360,10 +366,10 @@ int launch_update_tmap(const UtBlocks& blk, const cplx* C, int ldc, int r, const
         return -1;
       for (int j = 0; j < blk.nc[k]; j++) mp.crow[col + j] = blk.crow[k][j];
     }
-    col += (blk.nc[k] + 3) & ~3;
+    col += (blk.nc[k] + PC_UT_ALIGN - 1) / PC_UT_ALIGN * PC_UT_ALIGN;
     if (k == 0) mp.split = col;
   }
-  mp.pe = std::max(col, 4);
+  mp.pe = std::max((col + 3) & ~3, 4);
   if (mp.pe > 80 || r > 32) return -1;
   UtOut yo;
   yo.ld = blk.ld;
