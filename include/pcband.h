@@ -188,6 +188,10 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  wanted columns; -1: all b columns)
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
  *                  Diagonal/Trivial mode); 0: 7-pass pipeline with the standalone stencil
+ *   "plane_fuse"   1: at n = 128 the y-inverse, x-inverse + M_eps + x-forward and y-forward passes of
+ *                  a z-plane-local medium run as one pass over thread-block clusters of 8 CTAs
+ *                  (plane.cu: 3 HBM passes per apply instead of 5; measured slower: 3.14 vs 1.98 ms
+ *                  per 15 columns); 0 (default): the three passes
  *   "fuse_resid"   1 (default): both block updates + next residual + K_P^{-1} in one pass; 0: two
  *                  update launches and a separate residual pass
  *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)

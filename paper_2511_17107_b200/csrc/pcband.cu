@@ -149,6 +149,7 @@ struct pc_ctx {
   int sticky_lock = 0;         // 1: locked columns stay locked (SciPy's activeMask &=); 0: may re-activate
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
+  int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane.cu; measured slower)
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
@@ -467,6 +468,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "sticky_lock") c->sticky_lock = (int)v;
   else if (k == "gram_refresh") c->gram_refresh = (int)v;
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
+  else if (k == "plane_fuse") c->plane_fuse = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
@@ -606,6 +608,14 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
       while (nzc < n && n % nzc) nzc--;  // divisor of n
       nzc = std::min(nzc, n);
     }
+    if (c->plane_fuse && c->chunk_mb <= 0 && plane_supported(n)) {
+      // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane.cu)
+      const double cp = (double)nc * n * n * n;
+      const double cfl = 15.0 * std::log2((double)n) * cp;
+      Prof p(c, PC_STAT_EPS, st, 1, 4 * cfl + 100.0 * cp, 97.0 * cp);
+      cudaError_t e = launch_plane(n, c->eps_mode, Yc, WS, nc, c->d_mask, c->ec, c->d_tw, st);
+      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("plane pass: ") + cudaGetErrorString(e));
+    } else {
     const int ccols = nc;
     for (int j0 = 0; j0 < nc; j0 += ccols) {
       const int cn = std::min(ccols, nc - j0);
@@ -635,6 +645,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
           CHK(fft_pass(c, 1, -1, 0, Ws, Wm, none, cn, 1.0, st, z0, nz));
         }
       }
+    }
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);

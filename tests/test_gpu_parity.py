@@ -144,12 +144,15 @@ def test_apply_gamma_override_and_ld(api):
 
 
 # ------------------------------------------------------------------- full size (bench config)
-def test_apply_full_size_n128_fcc_pseudochiral(api):
-    """BASELINE config C4 at full size, the bench's launch configuration (a 15-column block)."""
+@pytest.mark.parametrize("plane", [1, 0])
+def test_apply_full_size_n128_fcc_pseudochiral(api, plane):
+    """BASELINE config C4 at full size, the bench's launch configuration (a 15-column block), with the
+    fused cluster plane pass (plane.cu) and with the three-pass middle section."""
     W = synth.WORKLOADS["C4"]
     n, A, e, masks = W.n, W.A(), W.eps1(), W.masks()
     k = np.array([PI, PI, PI])
     ctx = api.pc_create(A, n, e, masks)
+    api.pc_set_option(ctx, "plane_fuse", plane)
     x = np.concatenate([synth.random_block(n, 1, seed=21), synth.random_block(n, 1, seed=22, kind="smooth")])
     X = torch.zeros(15, 3 * n ** 3, dtype=torch.complex128, device="cuda")
     X[:2] = to_dev(x)
@@ -159,6 +162,28 @@ def test_apply_full_size_n128_fcc_pseudochiral(api):
     op = O.PenalizedOperator(n, k, A, e, masks)
     ref = op.apply_fourier(x)
     assert relerr_cols(Y[:2].cpu().numpy(), ref) <= 1e-12
+
+
+@pytest.mark.parametrize("mode,eps,geo", [("diagonal", "iso", "sphere"), ("trivial", "sdd", "random"),
+                                           ("crossdof", "pc", "random")])
+def test_apply_plane_pass_n128_modes(api, mode, eps, geo):
+    """The cluster plane pass (n = 128) in every mode it serves against the oracle (one white column),
+    and against the three-pass middle section on a 4-column block (<= 1e-13)."""
+    n = 128
+    A = synth.lattice("sc")
+    e = {"pc": synth.eps_pseudochiral(), "sdd": synth.eps_sdd(), "iso": synth.eps_isotropic(13.0)}[eps]
+    masks = synth.make_masks(geo, A, n, seed=5)
+    k = np.array([0.3, -1.2, 2.0])
+    ctx = api.pc_create(A, n, e, masks, eps_mode=mode)
+    X = torch.randn(4, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    Y1, Y0 = torch.empty_like(X), torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y1)
+    api.pc_set_option(ctx, "plane_fuse", 0)
+    api.pc_apply(ctx, k, X, Y0)
+    assert relerr_cols(Y1.cpu().numpy(), Y0.cpu().numpy()) <= 1e-13
+    op = O.PenalizedOperator(n, k, A, e, masks, mode)
+    ref = op.apply_fourier(X[:1].cpu().numpy())
+    assert relerr_cols(Y1[:1].cpu().numpy(), ref) <= 1e-12
 
 
 def _kappa2_closed(n, k, A):
