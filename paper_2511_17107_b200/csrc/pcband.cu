@@ -1150,7 +1150,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
       launch_rr(dG, p, b, c->drop_tol, dC, dLam, dInfo, dScr, st);
     }
-    cudaMemcpyAsync(hInfo, dInfo, 3 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(hInfo, dInfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
     if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("rayleigh-ritz: ") + cudaGetErrorString(e));
     return hInfo[0];  // rank
@@ -1250,8 +1250,9 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (j < nev && !(res[j] <= tol)) conv = 0;
     }
     if (c->verbose) {
-      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d |X|-1 %.1e cancel %.1e fb %d res:", kidx, it,
-              rank, hInfo[2], hInfo[1], xdev, last_cancel, c->derive_fallbacks);
+      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d |X|-1 %.1e cancel %.1e fb %d rr-cycles %d %d %d %d %d res:",
+              kidx, it, rank, hInfo[2], hInfo[1], xdev, last_cancel, c->derive_fallbacks, hInfo[3], hInfo[4],
+              hInfo[5], hInfo[6], hInfo[7]);
       for (int j = 0; j < b; j++) fprintf(stderr, " %.2e%s", res[j], active[j] ? "" : "*");
       fprintf(stderr, "\n");
     }

@@ -18,7 +18,6 @@ struct JacSm {
   int P[RR_MAXN / 2], Q[RR_MAXN / 2];
   double c[RR_MAXN / 2], s[RR_MAXN / 2];
   cplx e[RR_MAXN / 2];
-  int nrot;
 };
 
 DEV void tpair(int r, int i, int m, int& P, int& Q) {
@@ -33,32 +32,37 @@ DEV void tpair(int r, int i, int m, int& P, int& Q) {
 DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps, double rel_tol = 1e-16) {
   const int tid = threadIdx.x;
   const int h = np / 2;
+  const double tol2 = rel_tol * rel_tol;
   int sweep = 0;
   for (; sweep < max_sweeps; sweep++) {
-    if (tid == 0) js.nrot = 0;
-    __syncthreads();
+    int swept = 0;  // any rotation in this sweep (CTA-uniform)
     for (int r = 0; r < np - 1; r++) {
+      int rot = 0;
       for (int i = tid; i < h; i += blockDim.x) {
         int P, Q;
         tpair(r, i, np, P, Q);
         double c = 1.0, s = 0.0;
         cplx e = mk(1.0, 0.0);
         if (Q < n) {
-          cplx apq = A[P + Q * ld];
-          double mag = hypot(apq.x, apq.y);
-          double app = A[P + P * ld].x, aqq = A[Q + Q * ld].x;
-          if (mag > 1e-300 && mag > rel_tol * sqrt(fabs(app * aqq))) {
-            double z = (aqq - app) / (2.0 * mag);
-            double t = (z >= 0.0 ? 1.0 : -1.0) / (fabs(z) + sqrt(1.0 + z * z));
-            c = 1.0 / sqrt(1.0 + t * t);
+          // rotation zeroing a_pq with one reciprocal square root per quantity (no divisions by |a_pq|):
+          // e = a_pq / |a_pq|, z = (a_qq - a_pp) / (2 |a_pq|), t = sign(z) / (|z| + sqrt(1 + z^2)),
+          // c = 1 / sqrt(1 + t^2), s = t c
+          const cplx apq = A[P + Q * ld];
+          const double m2 = fma(apq.x, apq.x, apq.y * apq.y);
+          const double app = A[P + P * ld].x, aqq = A[Q + Q * ld].x;
+          if (m2 > 0.0 && m2 > tol2 * fabs(app * aqq)) {
+            const double rm = rsqrt(m2);
+            const double z = 0.5 * (aqq - app) * rm;
+            const double t = copysign(1.0, z) / (fabs(z) + sqrt(fma(z, z, 1.0)));
+            c = rsqrt(fma(t, t, 1.0));
             s = t * c;
-            e = mk(apq.x / mag, apq.y / mag);
-            atomicAdd(&js.nrot, 1);
+            e = mk(apq.x * rm, apq.y * rm);
+            rot = 1;
           }
         }
         js.P[i] = P; js.Q[i] = Q; js.c[i] = c; js.s[i] = s; js.e[i] = e;
       }
-      __syncthreads();
+      swept |= __syncthreads_or(rot);
       for (int it = tid; it < h * h; it += blockDim.x) {
         const int i = it % h, i2 = it / h;
         const double c = js.c[i], s = js.s[i], c2 = js.c[i2], s2 = js.s[i2];
@@ -90,9 +94,7 @@ DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_
       }
       __syncthreads();
     }
-    const int nr = js.nrot;
-    __syncthreads();
-    if (nr == 0) break;
+    if (!swept) break;
   }
   return sweep;
 }
@@ -148,6 +150,14 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   __shared__ int keep[RR_MAXN], order[RR_MAXN];
   __shared__ int rank_sh, chol_flag;
   const int tid = threadIdx.x;
+#ifdef PC_RR_TIMING
+  long long t_[8];
+  int nt_ = 0;
+#define RR_STAMP() do { if (tid == 0) t_[nt_] = clock64(); nt_++; } while (0)
+#else
+#define RR_STAMP() do { } while (0)
+#endif
+  RR_STAMP();
   const cplx* GM = G;
   const cplx* GA = G + (size_t)p * p;
   cplx* T = scratch;                                   // p x RR_MAXN
@@ -170,7 +180,9 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   __syncthreads();
 
   // 2a. fast path: Cholesky D G_M D = L L^H (pivots above drop_tol), H = L^{-1} D G_A D L^{-H}
+  RR_STAMP();
   const bool chol = cholesky_smem(A, p, ld, drop_tol, &chol_flag);
+  RR_STAMP();
   int r = p;
   int rp = np;
   if (chol) {
@@ -277,7 +289,9 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
     __syncthreads();
   }
   // 3. eig of H (r x r, ld rp)
+  RR_STAMP();
   int sw = jacobi_smem(A, V, r, rp, rp, js, 40, jtol);
+  RR_STAMP();
   for (int i = tid; i < r; i += blockDim.x) sig[i] = A[i + i * rp].x;
   __syncthreads();
   rank_sort(sig, r, order);
@@ -314,10 +328,15 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
     }
   }
   for (int t = tid; t < nout; t += blockDim.x) lam[t] = sig[order[t]];
+  RR_STAMP();
   if (tid == 0) {
     info[0] = r;
     info[1] = sw;
     info[2] = chol ? 1 : 0;
+    for (int i = 3; i < 8; i++) info[i] = 0;
+#ifdef PC_RR_TIMING  // per-phase clock64 cycles: scaling, Cholesky, H formation, Jacobi, back substitution
+    for (int i = 1; i < nt_ && i < 6; i++) info[3 + i - 1] = (int)(t_[i] - t_[i - 1]);
+#endif
   }
 }
 
