@@ -218,7 +218,7 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
 #define PC_GRAM40_KC 16
 #endif
 #ifndef PC_GRAM40_ST
-#define PC_GRAM40_ST 3
+#define PC_GRAM40_ST 4
 #endif
 static double g_grid_frac = 1.0;
 void set_grid_frac(double f) { g_grid_frac = (f > 0.0 && f <= 1.0) ? f : 1.0; }
