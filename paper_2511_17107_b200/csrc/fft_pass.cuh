@@ -116,6 +116,9 @@ struct TileMap {
 // Persistent, double-buffered pass: CTA b processes tiles b, b + G, b + 2G, ...; the next tile streams
 // into the other shared-memory stage (cp.async) while the current one is transformed and written.
 // Tile index t -> (tile in volume t % TPV, column/component t / TPV).
+#ifndef PC_KAG_PREFETCH
+#define PC_KAG_PREFETCH 0  // 1: last pass loads g before the DFTs (see fft_pass_kernel)
+#endif
 #ifndef PC_FFT_BOUNDS
 #define PC_FFT_BOUNDS 0  // 1: min-blocks launch bounds (4 CTAs/SM for the symbol passes, 3 for the plain ones)
 #endif
@@ -175,6 +178,17 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
 #pragma unroll
       for (int i = 0; i < 3; i++) kxy[i] = ldg(a.ktab + 3 * i * N + m1) + ldg(a.ktab + (3 * i + 1) * N + m2);
     }
+#if PC_KAG_PREFETCH
+    // OP_KAG: the penalty scalars g of this thread's elements are loaded before the DFTs (registers),
+    // so their latency overlaps the transform instead of the epilogue
+    cplx gpre[(OP == OP_KAG) ? (N * TP) / NT : 1];
+    if constexpr (OP == OP_KAG) {
+      const int cc0 = t / TPV;
+      const cplx* gkx0 = xh.p[(C == 3) ? cc0 : cc0 / 3];
+#pragma unroll
+      for (int q = 0; q < (N * TP) / NT; q++) gpre[q] = ldg(gkx0 + tm.off(tid / TP + q * (NT / TP), tid % TP));
+    }
+#endif
     cp_async_wait<1>();
     __syncthreads();
 
@@ -248,9 +262,14 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
       // loaded for all EPT elements first so the global latencies overlap
       const cplx* gkx = xh.p[col];
       const int p = tid % TP;
+#if PC_KAG_PREFETCH
+      const cplx* g = gpre;
+      (void)gkx;
+#else
       cplx g[EPT];
 #pragma unroll
       for (int q = 0; q < EPT; q++) g[q] = ldg(gkx + tm.off(tid / TP + q * (NT / TP), p));
+#endif
 #pragma unroll
       for (int q = 0; q < EPT; q++) {
         const int j = tid / TP + q * (NT / TP);
