@@ -167,6 +167,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "start"        0: Gaussian start block; 1 (default): transverse plane waves of the b/2 modes
  *                  with the smallest |kappa|^2 (eigenvectors of K_P) plus a seeded Gaussian admixture
  *   "start_noise"  relative size of that admixture (default 1e-3)
+ *   "start_precond" 1 (default): the admixture is K_P^{-1} of white noise (low modes only, small
+ *                  residual); 0: white Gaussian noise
  *   "sticky_lock"  1: a locked column stays locked; 0 (default): it re-enters the search block if
  *                  its residual rises above tol again
  *   "gram_refresh" every n-th iteration forms the full Gram matrices instead of using

@@ -164,7 +164,11 @@ struct pc_ctx {
   int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
   double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
-  double start_noise = 1e-3;   // plane-wave start: relative Gaussian admixture per column
+  int start_precond = 1;       // plane-wave start: Gaussian admixture through K_P^{-1} (see solve_k)
+#ifndef PC_START_NOISE
+#define PC_START_NOISE 1e-3
+#endif
+  double start_noise = PC_START_NOISE;  // plane-wave start: relative Gaussian admixture per column
   int warm_start = 0;          // 1: start from the previous k-point's Ritz vectors (same context, k != 0)
   int have_prev = 0, prev_slot = 0, prev_b = 0;
   DevBuf pwbuf;
@@ -488,6 +492,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "update_compact") set_update_compact((int)v);
   else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
+  else if (k == "start_precond") c->start_precond = (int)v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
   return PC_OK;
 }
@@ -1170,12 +1175,22 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       CU(cudaMemcpyAsync(col(sX, 0), col(c->prev_slot, 0), (size_t)b * colb, cudaMemcpyDeviceToDevice, st));
   } else {
     const bool pw = c->start_mode == 1;
-    const double noise = pw ? c->start_noise / std::sqrt((double)len) : 1.0;
-    Prof pf(c, PC_STAT_OTHER, st, pw ? 3 : 1, 0.0, 16.0 * len * b);
+    // start_precond: the admixture is K_P^{-1} g (g white, scaled by 4 pi^2 so that its lowest modes keep
+    // the white admixture's amplitude): every low mode is seeded (degenerate and spurious gamma-modes
+    // are found), but without the white noise's high-|kappa| content, whose residual (~ noise x max
+    // |kappa|^2 ~ 1e4 at n = 128) the first iterations otherwise spend their time removing
+    const bool pre = pw && c->start_precond && c->start_noise > 0.0;
+    const double noise = pw ? c->start_noise / std::sqrt((double)len) * (pre ? 4.0 * M_PI * M_PI : 1.0) : 1.0;
+    Prof pf(c, PC_STAT_OTHER, st, pw ? (pre ? 4 : 3) : 1, 0.0, 16.0 * len * b);
     MutColPtrs x0;
     mcols(sX, all, x0, 0);
     launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)kidx), deflate ? (int)c->n3 : 0,
                  noise, st);
+    if (pre) {
+      ColPtrs xi;
+      ccols(sX, all, xi, 0);
+      launch_precond(xi, x0, b, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, st);
+    }
     if (pw) CHK(plane_wave_start(c, x0, b, st));
   }
   CHK(apply_list(sX, sAX, all));
