@@ -151,6 +151,8 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane.cu; measured slower)
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
+  int tail_guard = 0;          // > 0: once at most tail_at wanted columns are unconverged, this many more
+  int tail_at = 3;             //      guard columns (after nev + w_guard) also get W (see solve_k)
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
   int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
   int gram_tmap = 0;           // 1: Gram S^H [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu; slower)
@@ -474,6 +476,8 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "plane_fuse") c->plane_fuse = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
+  else if (k == "tail_guard") c->tail_guard = (int)v;
+  else if (k == "tail_at") c->tail_at = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
   else if (k == "gram_herm") c->gram_herm = (int)v;
@@ -1222,7 +1226,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   std::vector<double> res(b, 0.0);
   c->hist.clear();
   c->hist_b = b;
-  bool haveP = false, resid_ready = false;
+  bool haveP = false, resid_ready = false, tail_on = false;
   c->derive_fallbacks = 0;
   int it = 0, conv = 0;
   // trim_locked: the update writes W', P', AP' only for the columns that are active in this iteration
@@ -1253,15 +1257,24 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     double xdev = 0.0;  // X^H X = I is assumed by the Gram assembly; its diagonal is measured here
     for (int j = 0; j < b; j++) xdev = std::max(xdev, std::fabs(hN[2 * j + 1] - 1.0));
     force_full = !(xdev <= c->xdev_tol);
+    for (int j = 0; j < b; j++) res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
+    if (c->tail_guard > 0 && c->w_guard >= 0 && !ug_ok && !tail_on) {
+      // the slowest wanted columns converge at a rate set by their gap to the guard Ritz values; the
+      // guard columns that never get W stay poor (Res ~ 1e1), so in the tail the first tail_guard of
+      // them get search directions too (cheap then: few wanted columns are still active)
+      int nun = 0;
+      for (int j = 0; j < nev; j++) nun += (res[j] > tol) ? 1 : 0;
+      tail_on = nun <= c->tail_at;
+    }
+    const int wlim = (c->w_guard < 0) ? b : std::min(b, nev + c->w_guard + (tail_on ? c->tail_guard : 0));
     for (int j = 0; j < b; j++) {
-      res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
       c->hist.push_back(res[j]);
       // soft locking: a converged column leaves the search block (no W, P); with sticky_lock = 0 it
       // re-enters if its residual rises above tol again
       if (!(res[j] > tol)) active[j] = 0;
       else if (!c->sticky_lock) active[j] = 1;
       // guard columns beyond nev + w_guard never get a search direction (they ride along in X and P)
-      if (c->w_guard >= 0 && j >= nev + c->w_guard) active[j] = 0;
+      if (j >= wlim) active[j] = 0;
       if (j < nev && !(res[j] <= tol)) conv = 0;
     }
     if (c->verbose) {

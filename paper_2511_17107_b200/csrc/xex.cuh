@@ -37,7 +37,16 @@ struct XexCfg {
 // First Stockham step for npen rows: R2 DFTs of size R1 (input stride R2) + twiddles, result in the
 // mid layout of the row.  Input element j of pencil pen comes from load(pen, j) (global or shared).
 // Thread item = (pen, j2) with j2 fastest: R2 lanes read R2 consecutive inputs of one pencil.
-template <int N, int DIR, class Load, class Row>
+// TT: tw is the transposed table tw[k1 R2 + j2] = W_N^{j2 k1} (xrow_twiddles), so that the R2 lanes of
+// one pencil read consecutive twiddles (the natural table tw[(j2 k1) % N] is a stride-k1 read: up to
+// 8-way bank conflicts on the 16-B loads).
+template <int N>
+DEV void xrow_twiddles(cplx* tw, const cplx* __restrict__ twg) {
+  constexpr int R2 = XRow<N>::R2;
+  for (int j = threadIdx.x; j < N; j += blockDim.x) tw[j] = ldg(twg + ((j % R2) * (j / R2)) % N);
+}
+
+template <int N, int DIR, class Load, class Row, bool TT = false>
 DEV void xrow_step1(cplx* s, const cplx* tw, int npen, Load load, Row row, bool sync_inplace) {
   using X = XRow<N>;
   constexpr int R1 = X::R1, R2 = X::R2, S1 = X::S1, P = X::P;
@@ -57,7 +66,7 @@ DEV void xrow_step1(cplx* s, const cplx* tw, int npen, Load load, Row row, bool 
       cplx* d = s + row(pen) * P + j2 * S1;
 #pragma unroll
       for (int k1 = 0; k1 < R1; k1++) {
-        cplx w = tw[(j2 * k1) % N];
+        cplx w = TT ? tw[k1 * R2 + j2] : tw[(j2 * k1) % N];
         if (DIR > 0) w.y = -w.y;
         d[k1] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
       }
@@ -138,11 +147,12 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
       mk8[e] = __ldg(mask + ((long long)z * N + y) * N + j);
     }
   }
-  for (int j = tid; j < N; j += NT) tw[j] = ldg(twg + j);
+  xrow_twiddles<N>(tw, twg);
   __syncthreads();
 
   // inverse x-DFT of the held rows: first step straight from HBM (R2 lanes read R2 consecutive complex)
-  xrow_step1<N, +1>(s, tw, NPEN, [&](int pen, int j) { return ldg(gin + grow(prow(pen)) + j); }, prow, false);
+  auto gload = [&](int pen, int j) { return ldg(gin + grow(prow(pen)) + j); };
+  xrow_step1<N, +1, decltype(gload), decltype(prow), true>(s, tw, NPEN, gload, prow, false);
   __syncthreads();
   xrow_step2<N, +1>(s, NPEN, [&](int pen, int k, cplx v) { s[prow(pen) * P + k] = v; }, prow, true);
   if constexpr (N % 16 == 0) cp_async_wait<0>();
@@ -209,7 +219,8 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
 
   // forward x-DFT of the TP output rows; the last step writes HBM directly (R1 consecutive complex)
   auto orow = [](int pen) { return (pen / TP) * RP + 1 + pen % TP; };
-  xrow_step1<N, -1>(s, tw, 3 * TP, [&](int pen, int j) { return s[orow(pen) * P + j]; }, orow, true);
+  auto sload = [&](int pen, int j) { return s[orow(pen) * P + j]; };
+  xrow_step1<N, -1, decltype(sload), decltype(orow), true>(s, tw, 3 * TP, sload, orow, true);
   xrow_step2<N, -1>(s, 3 * TP, [&](int pen, int k, cplx v) {
     const int c = pen / TP, r = pen % TP;
     gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + k] = v;

@@ -23,12 +23,15 @@ ap.add_argument("--values", type=float, nargs="+", required=True)
 ap.add_argument("--nk", type=int, default=2)
 ap.add_argument("--tol", type=float, default=1e-5)
 ap.add_argument("--maxit", type=int, default=1000)
+ap.add_argument("--set", nargs="*", default=[], help="fixed options key=value applied first")
 a = ap.parse_args()
 W = synth.WORKLOADS[a.workload]
 A = W.A()
 masks = synth.make_masks(W.geometry, A, W.n)
 kp = synth.kpath(W.lattice, W.segments)[1: 1 + a.nk]
 ctx = api.pc_create(A, W.n, W.eps1(), masks)
+for kv in a.set:
+    api.pc_set_option(ctx, kv.split("=")[0], float(kv.split("=")[1]))
 api.pc_bands(ctx, kp[:1], nev=W.nev, tol=a.tol, maxit=20)  # warm-up
 out = {}
 for v in a.values:
