@@ -180,12 +180,18 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+PRECOND_DESC = {"kp": "K_P^{-1}, the paper's FFT-diagonal preconditioner (PAPER.md:530-548)",
+                "eps": "eps-weighted K_P^{-1}: K_A^+H diag(M_eps)^{-1} K_A^+ + Pi/(gamma|kappa|^2) "
+                       "(beyond the paper, DESIGN.md R16)"}
+
+
 def workload_config(W, args):
     return {"workload": f"{W.name}: {W.lattice.upper()} lattice, {W.geometry} inclusion, eps1={W.eps} "
                         f"(pseudochiral eps_lat=13 beta=0.875, PAPER.md:1083-1093), n={W.n}, {W.nev} bands, "
                         f"tol={args.tol:g}, k-path {len(W.kpoints())} points",
             "n": W.n, "nev": W.nev, "block": W.nev + (args.guard if args.guard is not None else 6), "tol": args.tol, "lattice": W.lattice,
             "geometry": W.geometry, "eps_mode": "crossdof",
+            "precond": PRECOND_DESC[getattr(args, "precond", "kp")],
             "l2": "no flush: per-k working set ~15 GB >> 126 MB L2",
             "start": ("warm: each context solves a contiguous k stretch, k_i started from k_(i-1)'s Ritz block "
                       "(SURVEY f2, not the paper's protocol)") if getattr(args, "warm_start", False)
@@ -213,6 +219,11 @@ def main():
     ap.add_argument("--warm-start", action="store_true",
                     help="path continuation: contiguous k stretches per context, each k started from the "
                          "previous k's Ritz block (SURVEY f2; not the paper's cold start, reported separately)")
+    ap.add_argument("--precond", default="kp", choices=["kp", "eps"],
+                    help="kp: the paper's K_P^{-1} (P:530-548, default, the headline); eps: the eps-weighted "
+                         "preconditioner (beyond the paper, DESIGN R16)")
+    ap.add_argument("--no-alt", action="store_true",
+                    help="skip the secondary timed run with the other preconditioner (key alt_precond)")
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + ranks sharing GPUs (rank -> device rank %% count): a functional test of the "
                          "multi-rank path on a smaller box; numbers from it are not scaling results")
@@ -256,6 +267,7 @@ def main():
             api.pc_set_option(c_, "guard", args.guard)
         if args.w_guard is not None:
             api.pc_set_option(c_, "w_guard", args.w_guard)
+        api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
     ctx = ctxs[0]
 
     def kidx(s):
@@ -316,6 +328,32 @@ def main():
         out = torch.empty((world * loc.shape[0], loc.shape[1]), dtype=loc.dtype, device=cdev)
         dist.all_gather_into_tensor(out, loc)
         gathered = out.shape[0]
+
+    # ---- the same timed steps with the other preconditioner (same k-points, same protocol), reported
+    # under alt_precond: the headline stays on the paper's K_P^{-1} unless --precond eps
+    alt = None
+    if not args.no_alt and not args.warm_start:
+        other = "eps" if args.precond == "kp" else "kp"
+        for c_ in ctxs:
+            api.pc_set_option(c_, "precond", 1 if other == "eps" else 0)
+        run([kidx(s) for s in range(len(ctxs))])  # one untimed solve per context
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record()
+        aom, ars, ait, ast = run(idx)
+        a1.record()
+        torch.cuda.synchronize()
+        ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=cdev)
+        if world > 1:
+            dist.all_reduce(ta, op=dist.ReduceOp.MAX)
+        barrier()
+        for c_ in ctxs:
+            api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
+        alt = {"precond": PRECOND_DESC[other], "value": world * args.steps / (float(ta.item()) / 1000.0),
+               "unit": "k-points/s", "ms_per_step": float(ta.item()) / args.steps,
+               "iters": [int(v) for v in ait], "status": [int(v) for v in ast],
+               "max_rel_diff_omega2_vs_headline": float(np.max(np.abs(aom - om) / np.abs(om))),
+               "note": "same k-points and protocol as the headline steps, timed right after them"}
 
     # ---- pc_apply bandwidth (second half of the metric): a b-column block at n=128
     ncol = args.apply_cols
@@ -435,6 +473,7 @@ def main():
                     api.pc_set_option(c_, "guard", args.guard)
                 if args.w_guard is not None:
                     api.pc_set_option(c_, "w_guard", args.w_guard)
+                api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
             if nctx == 1:
                 out = bands.solve_local(ce[0], kp, idx_list, W.nev, args.tol, args.maxit, 0)
             else:
@@ -491,7 +530,7 @@ def main():
                 "config": workload_config(W, args) | {"kpoints_per_rank": args.steps,
                                                       "parallelism": f"k-path sharded over {world} GPU(s), "
                                                                      f"{len(ctxs)} concurrent k-point solve(s) per GPU"},
-                "iters": iters, "status": status, "warmup_iters": wit,
+                "iters": iters, "status": status, "warmup_iters": wit, "alt_precond": alt,
                 "omega2_first_k": om[0].tolist(), "resid_max": float(rs.max()),
                 "apply": apply, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": stats["launches"], "clocks": clocks,

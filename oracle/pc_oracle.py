@@ -36,6 +36,7 @@ __all__ = [
     "circulant_D1", "circulant_D0", "circulant_symbols", "dft_matrix", "axis_embed",
     "shifted_blocks", "curl_matrix", "div_matrix", "transfer_T", "permittivity_matrix",
     "gamma_rule", "PenalizedOperator", "symbols_1d", "kappa_symbols", "precond_fourier",
+    "precond_eps_fourier",
     "hpd_report", "eigs_dense", "eigs_iterative", "fft3_fourier_to_real",
     "fft3_real_to_fourier",
 ]
@@ -311,6 +312,44 @@ def precond_fourier(n: int, k, A, gamma: float, R: np.ndarray) -> np.ndarray:
     for c in range(Rb.shape[0]):
         v = Rb[c].reshape(3, -1).T[:, :, None]
         out[c] = np.linalg.solve(KP, v)[:, :, 0].T.reshape(-1)
+    return out.reshape(np.shape(R))
+
+
+def precond_eps_fourier(n: int, k, A, gamma: float, eps1, masks, mode: str, R: np.ndarray) -> np.ndarray:
+    """eps-weighted preconditioner (BEYOND THE PAPER: the paper's preconditioner is K_P^{-1},
+    P:530-548; this is the Maxwell-solver variant that weights the two curl halves by the medium,
+    reading R16 in DESIGN.md).  Per column r (Fourier coordinates):
+
+        T r = K_A^{+H} F3^H D^{-1} F3 K_A^{+} r + Pi r / (gamma |kappa|^2)
+
+    with K_A = [kappa]_x, its pseudo-inverse K_A^+ = K_A^H / |kappa|^2, the projector
+    Pi = conj(kappa) kappa^T / |kappa|^2 onto the range of K_B, F3 = ifftn and
+    D = the diagonal of the oracle's own M_eps (permittivity_matrix).  Modes with
+    |kappa|^2 <= 1e-28 max|kappa|^2 map to 0.  R: (ncols, 3N^3)."""
+    kap = kappa_symbols(n, k, A).reshape(3, -1)           # (3, N^3)
+    k2 = np.sum(np.abs(kap) ** 2, axis=0)
+    zero = k2 <= 1e-28 * k2.max()
+    k2s = np.where(zero, 1.0, k2)
+    nm = kap.shape[1]
+    # explicit 3x3 matrices per mode
+    KA = np.zeros((nm, 3, 3), dtype=np.complex128)
+    KA[:, 0, 1], KA[:, 0, 2] = -kap[2], kap[1]
+    KA[:, 1, 0], KA[:, 1, 2] = kap[2], -kap[0]
+    KA[:, 2, 0], KA[:, 2, 1] = -kap[1], kap[0]
+    KAp = np.conj(np.transpose(KA, (0, 2, 1))) / k2s[:, None, None]      # K_A^+
+    KApH = np.conj(np.transpose(KAp, (0, 2, 1)))                          # K_A^{+H}
+    Pi = np.conj(kap).T[:, :, None] * kap.T[:, None, :] / k2s[:, None, None]
+    Dinv = 1.0 / permittivity_matrix(eps1, masks, mode).diagonal()
+    Rb = np.atleast_2d(R)
+    out = np.empty_like(Rb, dtype=np.complex128)
+    for c in range(Rb.shape[0]):
+        r = Rb[c].reshape(3, -1).T[:, :, None]                            # (N^3, 3, 1)
+        u = (KAp @ r)[:, :, 0].T.reshape(-1)                              # K_A^+ r
+        H = fft3_fourier_to_real(u, n) * Dinv                             # D^{-1} F3 (.)
+        s = fft3_real_to_fourier(H, n).reshape(3, -1).T[:, :, None]       # F3^H (.)
+        y = (KApH @ s)[:, :, 0] + (Pi @ r)[:, :, 0] / (gamma * k2s[:, None])
+        y[zero] = 0.0
+        out[c] = y.T.reshape(-1)
     return out.reshape(np.shape(R))
 
 

@@ -279,6 +279,13 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
         cplx y1 = cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), g[q]);
         cplx y2 = cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), g[q]);
         cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), g[q]);
+        if (a.kscale) {
+          const double kk = k1.x * k1.x + k1.y * k1.y + k2.x * k2.x + k2.y * k2.y + k3.x * k3.x + k3.y * k3.y;
+          const double inv = (kk > a.thr) ? 1.0 / kk : 0.0;
+          y1 = inv * y1;
+          y2 = inv * y2;
+          y3 = inv * y3;
+        }
         gout[o] = y1;
         gout[N3 + o] = y2;
         gout[2 * N3 + o] = y3;

@@ -151,6 +151,8 @@ struct pc_ctx {
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
   int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane.cu; measured slower)
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
+  int precond = 0;             // 0: K_P^{-1}; 1: eps-weighted K_P^{-1} (beyond the paper, see precond_eps)
+  EpsCoef ec_inv{};            // diagonal of M_eps inverted: 1/eps_ii - 1 on the masks I_i (precond = 1)
   int tail_guard = 0;          // > 0: once at most tail_at wanted columns are unconverged, this many more
   int tail_at = 3;             //      guard columns (after nev + w_guard) also get W (see solve_k)
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
@@ -358,6 +360,7 @@ extern "C" int pc_create(pc_ctx** out, const double A[9], int n, const double ep
   c->hpd_flags = (a1 ? PC_HPD_ASSUMP1 : 0) | (sdd ? PC_HPD_SDD : 0) | (zero_off ? PC_HPD_ZERO_OFFD : 0) |
                  ((a1 && (sdd || zero_off)) ? PC_HPD_GUARANTEED : 0);
   for (int i = 0; i < 3; i++) c->ec.d[i] = eps1[2 * (3 * i + i)] - 1.0;
+  for (int i = 0; i < 3; i++) c->ec_inv.d[i] = 1.0 / eps1[2 * (3 * i + i)] - 1.0;  // eps_ii > 0 (HPD, checked below)
   const int od[3][2] = {{0, 1}, {0, 2}, {1, 2}};
   for (int t = 0; t < 3; t++) {
     int i = od[t][0], j = od[t][1];
@@ -477,6 +480,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "plane_fuse") c->plane_fuse = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "tail_guard") c->tail_guard = (int)v;
+  else if (k == "precond") c->precond = (int)v;
   else if (k == "tail_at") c->tail_at = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
@@ -558,15 +562,27 @@ static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // apply
 // ------------------------------------------------------------------------------------------
+// The operator the apply pipeline runs: Op = K_A M K_A^H + gamma K_B (the paper's), or, for
+// the eps-weighted preconditioner, (1/|kappa|^2) (K_A D^{-1} K_A^H + K_B) with D = diag(M_eps) (precond_eps).
+struct ApplyOp {
+  int mode;            // PC_EPS_* of the middle factor
+  const EpsCoef* ec;   // its coefficients
+  int prec;            // 1: gamma = 1 and the last pass scales by 1/|kappa|^2
+};
+static ApplyOp paper_op(const pc_ctx* c) { return ApplyOp{c->eps_mode, &c->ec, 0}; }
+
 static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
-                    const ColPtrs& xh, int nc, double scale, cudaStream_t st, int z0 = 0, int nz = 0) {
+                    const ColPtrs& xh, int nc, double scale, cudaStream_t st, int z0 = 0, int nz = 0,
+                    int prec = 0) {
   PassArgsH a;
   a.tw = c->d_tw;
   a.ktab = c->d_ktab;
-  a.gamma = c->cur_gamma;
+  a.gamma = prec ? 1.0 : c->cur_gamma;
   a.scale = scale;
   a.z0 = z0;
   a.nz = nz;
+  a.kscale = (prec && kind == 2) ? 1 : 0;
+  a.thr = c->cur_thr;
   cudaError_t e = launch_fft_pass(c->n, axis, dir, kind, in, out, xh, nc, a, st);
   if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("fft pass: ") + cudaGetErrorString(e));
   return PC_OK;
@@ -580,7 +596,8 @@ static ColPtrs to_const(const MutColPtrs& m, int nc) {
 
 // Fourier-space apply of nc <= PC_MAXCOLS columns: Y = Op X, ws = nc workspace columns.
 static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const MutColPtrs& WS, int nc,
-                         cudaStream_t st) {
+                         cudaStream_t st, const ApplyOp* opp = nullptr) {
+  const ApplyOp op = opp ? *opp : paper_op(c);
   const int n = c->n;
   const double inv_n3 = 1.0 / ((double)n * n * n);
   ColPtrs Yc = to_const(Y, nc), Wc = to_const(WS, nc), none{};
@@ -598,11 +615,11 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   for (int j = 0; j < nc; j++) KX.p[j] = c->kxws.as<cplx>() + (size_t)j * c->n3;
   {
     Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 38.0 * pts, 112.0 * pts);
-    CHK(fft_pass(c, 2, +1, 1, X, Y, KX, nc, inv_n3, st));
+    CHK(fft_pass(c, 2, +1, 1, X, Y, KX, nc, inv_n3, st, 0, 0, op.prec));
   }
   // z-plane-local media (eps_13 = eps_23 = 0 in CrossDoF; any Diagonal/Trivial medium): the x-passes
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
-  const bool plane_local = c->fuse_xex && (c->eps_mode != PC_EPS_CROSSDOF || (!c->ec.has[1] && !c->ec.has[2]));
+  const bool plane_local = c->fuse_xex && (op.mode != PC_EPS_CROSSDOF || (!op.ec->has[1] && !op.ec->has[2]));
   if (plane_local) {
     // Middle passes (y-inverse, x-inverse + M_eps + x-forward, y-forward) in L2-sized chunks of
     // (column, z-planes): the chunk written by one pass is re-read by the next while it is still in
@@ -622,7 +639,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
       const double cp = (double)nc * n * n * n;
       const double cfl = 15.0 * std::log2((double)n) * cp;
       Prof p(c, PC_STAT_EPS, st, 1, 4 * cfl + 100.0 * cp, 97.0 * cp);
-      cudaError_t e = launch_plane(n, c->eps_mode, Yc, WS, nc, c->d_mask, c->ec, c->d_tw, st);
+      cudaError_t e = launch_plane(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
       if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("plane pass: ") + cudaGetErrorString(e));
     } else {
     const int ccols = nc;
@@ -646,7 +663,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
         }
         {
           Prof p(c, PC_STAT_EPS, st, 1, 2 * cfl + 100.0 * cp, 96.0 * cp);
-          cudaError_t e = launch_xex(n, c->eps_mode, Ys, Wm, cn, c->d_mask, c->ec, c->d_tw, 1.0, z0, nz, st);
+          cudaError_t e = launch_xex(n, op.mode, Ys, Wm, cn, c->d_mask, *op.ec, c->d_tw, 1.0, z0, nz, st);
           if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
         }
         {
@@ -658,7 +675,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
-      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st));
+      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec));
     }
     return PC_OK;
   }
@@ -669,7 +686,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   }
   {
     Prof p(c, PC_STAT_EPS, st, 1, 100.0 * pts, 97.0 * pts);
-    launch_eps(c->eps_mode, Yc, WS, nc, n, c->d_mask, c->ec, st);
+    launch_eps(op.mode, Yc, WS, nc, n, c->d_mask, *op.ec, st);
   }
   {
     Prof p(c, PC_STAT_FFT_MID, st, 2, 2 * fl, 2 * 96.0 * pts);
@@ -678,9 +695,23 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   }
   {
     Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
-    CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st));
+    CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec));
   }
   return PC_OK;
+}
+
+// eps-weighted preconditioner (beyond the paper; option precond = 1).  The paper's K_P^{-1} inverts
+// the vacuum symbol K_A K_A^H + gamma K_B.  This variant puts the inverse of M_eps's
+// diagonal D = diag(m_i), m_i = (eps_ii - 1) I_i + 1, between the two curl halves:
+//   T = (K_A / |kappa|^2) D^{-1} (K_A^H / |kappa|^2) + Pi / (gamma |kappa|^2),  Pi = conj(kappa) kappa^T / |kappa|^2,
+// which is K_P^{-1} in vacuum (D = I) and the exact inverse for a homogeneous medium.  Given
+// W0 = K_P^{-1} R (what the residual kernels write): K_A^H W0 = K_A^H R / |kappa|^2 and
+// kappa^T W0 = kappa^T R / (gamma |kappa|^2), so T R = (1/|kappa|^2) (K_A D^{-1} K_A^H + K_B) W0 --
+// the apply pipeline with D^{-1} in the middle, gamma = 1 and a 1/|kappa|^2 epilogue, in place on W.
+// Modes with |kappa|^2 <= thr map to 0.
+static int precond_eps(pc_ctx* c, const MutColPtrs& W, const MutColPtrs& WS, int nc, cudaStream_t st) {
+  const ApplyOp op{PC_EPS_DIAGONAL, &c->ec_inv, 1};
+  return apply_fourier(c, to_const(W, nc), W, WS, nc, st, &op);
 }
 
 // unitary 3-D DFT per component; dir = -1: F3^H (to Fourier), +1: F3 (to real).  Y may equal X.
@@ -786,8 +817,16 @@ extern "C" int pc_precond(pc_ctx* c, const double k[3], const void* R, void* P, 
     MutColPtrs p;
     block_ptrs(R, ld, j0, nc, r);
     block_ptrs(P, ld, j0, nc, p);
-    Prof pf(c, PC_STAT_RESID, st, 1, 60.0 * c->n3 * nc, 96.0 * c->n3 * nc);
-    launch_precond(r, p, nc, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, st);
+    {
+      Prof pf(c, PC_STAT_RESID, st, 1, 60.0 * c->n3 * nc, 96.0 * c->n3 * nc);
+      launch_precond(r, p, nc, c->n, c->d_ktab, c->cur_gamma, c->cur_thr, st);
+    }
+    if (c->precond == 1) {
+      CHK(ensure_ws(c, nc));
+      MutColPtrs w;
+      for (int j = 0; j < nc; j++) w.p[j] = c->ws.as<cplx>() + (size_t)j * c->len;
+      CHK(precond_eps(c, p, w, nc, st));
+    }
   }
   CU(cudaGetLastError());
   return PC_OK;
@@ -1154,6 +1193,13 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     for (size_t t = 0; t < js.size(); t++) w.p[t] = wsp.p[t];
     return apply_fourier(c, x, y, w, (int)js.size(), st);
   };
+  auto precond_list = [&](int slot, const std::vector<int>& js) -> int {  // W <- T R from W = K_P^{-1} R
+    MutColPtrs y;
+    mcols(slot, js, y, 0);
+    MutColPtrs w;
+    for (size_t t = 0; t < js.size(); t++) w.p[t] = wsp.p[t];
+    return precond_eps(c, y, w, (int)js.size(), st);
+  };
   auto rr = [&](int p) -> int {
     {
       Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
@@ -1308,6 +1354,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       for (int j : miss) hasW[j] = 1;
     }
     const int nP = (int)actP.size();
+    if (c->precond == 1) CHK(precond_list(WW, act));
     CHK(apply_list(WW, AWW, act));
     int p = 0;
     cplx* const dG0 = dG;  // the previous step's Gram (read by the derived assembly)

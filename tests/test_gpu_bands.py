@@ -221,7 +221,8 @@ def test_bands_warm_start_path_continuation(api):
                                   {"update_tma": 1}, {"gram_refresh": 1}, {"gram_herm": 1},
                                   {"update_compact": 1}, {"trim_locked": 0}, {"sticky_lock": 1},
                                   {"update_stream": 1}, {"gram_derive": 1}, {"update_tmap": 1},
-                                  {"update_tmap": 0}, {"gram_tmap": 0}, {"gram_tmap": 1, "sticky_lock": 1}])
+                                  {"update_tmap": 0}, {"gram_tmap": 0}, {"gram_tmap": 1, "sticky_lock": 1},
+                                  {"precond": 1}, {"precond": 1, "trim_locked": 0}, {"tail_guard": 3, "tail_at": 5}])
 def test_bands_option_variants(api, opts):
     """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
     tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""

@@ -79,6 +79,32 @@ def test_precond_matches_oracle(api, lat, n, k):
     assert relerr_cols(P.cpu().numpy(), ref) <= 1e-12
 
 
+PRECOND_EPS_CASES = [
+    ("fcc", "fcc_diamond", "pc", "crossdof", 8, (PI, PI, PI)),
+    ("sc", "sphere", "iso", "crossdof", 12, (0.0, 0.0, 0.0)),
+    ("sc", "random", "sdd", "crossdof", 16, (0.3, -1.2, 2.5)),
+    ("bcc", "random", "pc", "trivial", 10, (2 * PI, 0, 0)),
+    ("fcc", "fcc_diamond", "pc", "crossdof", 128, (PI / 2, 2 * PI, PI / 2)),
+]
+
+
+@pytest.mark.parametrize("lat,geo,eps,mode,n,k", PRECOND_EPS_CASES)
+def test_precond_eps_matches_oracle(api, lat, geo, eps, mode, n, k):
+    """Option precond = 1 (eps-weighted preconditioner, reading R16): pc_precond against the oracle's
+    explicit per-mode formula, including k = 0 (zero mode -> 0) and the n = 128 bench grid."""
+    A = synth.lattice(lat)
+    e = _eps(eps)
+    masks = synth.make_masks(geo, A, n, seed=11)
+    ctx = api.pc_create(A, n, e, masks, eps_mode=mode)
+    api.pc_set_option(ctx, "precond", 1)
+    nc = 1 if n >= 64 else 2
+    r = synth.random_block(n, nc, seed=21)
+    P = torch.empty(nc, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    api.pc_precond(ctx, k, to_dev(r), P)
+    ref = O.precond_eps_fourier(n, np.array(k), A, O.gamma_rule(np.array(k)), e, masks, mode, r)
+    assert relerr_cols(P.cpu().numpy(), ref) <= 1e-12
+
+
 # ------------------------------------------------------------------------------------- apply
 APPLY_CASES = [
     ("sc", "random", "pc", "crossdof", 4, (PI, PI, PI)),

@@ -389,6 +389,52 @@ def test_preconditioner_inverts_vacuum_operator_P532(lat, k):
     assert np.allclose(O.precond_fourier(n, k, A, op.gamma, y), x, atol=1e-10)
 
 
+@pytest.mark.parametrize("lat,k", [("sc", (0.5, 0.2, -0.1)), ("fcc", (PI, PI, PI))])
+def test_eps_preconditioner_is_kp_in_vacuum(lat, k):
+    """With M = I the eps-weighted preconditioner (reading R16) reduces to the paper's K_P^{-1}
+    (P:530-548): (I - Pi)/|kappa|^2 + Pi/(gamma |kappa|^2)."""
+    n = 5
+    A = synth.lattice(lat)
+    k = np.array(k)
+    masks = synth.make_masks("vacuum", A, n)
+    g = O.gamma_rule(k)
+    r = synth.random_block(n, 2, seed=12)
+    ref = O.precond_fourier(n, k, A, g, r)
+    got = O.precond_eps_fourier(n, k, A, g, synth.eps_pseudochiral(), masks, "crossdof", r)
+    assert np.allclose(got, ref, rtol=0, atol=1e-12 * np.abs(ref).max())
+
+
+@pytest.mark.parametrize("lat,c", [("sc", 13.0), ("fcc", 0.2)])
+def test_eps_preconditioner_inverts_homogeneous_operator(lat, c):
+    """For a homogeneous isotropic medium (every mask 1, eps_1 = c I, so M = c I) the eps-weighted
+    preconditioner is the exact inverse of the Fourier-space operator: T Op x = x (k != 0, no zero
+    modes).  The check goes through the oracle's sparse operator, not the symbols."""
+    n = 4
+    A = synth.lattice(lat)
+    k = np.array([0.7, -1.1, 0.4])
+    masks = synth.make_masks("full", A, n)
+    op = O.PenalizedOperator(n, k, A, c * np.eye(3), masks, "crossdof")
+    x = synth.random_block(n, 2, seed=13)
+    y = op.apply_fourier(x)
+    got = O.precond_eps_fourier(n, k, A, op.gamma, c * np.eye(3), masks, "crossdof", y)
+    assert np.allclose(got, x, rtol=0, atol=1e-9 * np.abs(x).max())
+
+
+def test_eps_preconditioner_hermitian_positive():
+    """T is Hermitian positive definite on an inhomogeneous pseudochiral medium (k != 0):
+    <x, T y> = <T x, y>, <x, T x> > 0."""
+    n = 6
+    A = synth.lattice("fcc")
+    k = np.array([PI, PI, PI])
+    masks = synth.make_masks("fcc_diamond", A, n)
+    e = synth.eps_pseudochiral()
+    g = O.gamma_rule(k)
+    x, y = synth.random_block(n, 2, seed=14)
+    Tx, Ty = O.precond_eps_fourier(n, k, A, g, e, masks, "crossdof", np.stack([x, y]))
+    assert abs(np.vdot(x, Ty) - np.vdot(Tx, y)) <= 1e-12 * abs(np.vdot(x, Ty))
+    assert np.vdot(x, Tx).real > 0 and abs(np.vdot(x, Tx).imag) <= 1e-12 * np.vdot(x, Tx).real
+
+
 def test_kappa_symbols_match_operator():
     """kappa_i(m) are the eigenvalues of Dhat_i on the Fourier basis."""
     n = 4
