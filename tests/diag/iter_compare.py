@@ -1,7 +1,7 @@
 """LOBPCG iteration counts: SciPy's LOBPCG (oracle operator + oracle K_P^{-1}) vs pc_bands option
 variants, same operator, same k-points (Table 2 at P:1187-1203 for context).
 
-usage: python tools/iter_compare.py [--n 32] [--nk 4] [--which scipy,gpu] [--variants ...]
+usage: python tests/diag/iter_compare.py [--n 32] [--nk 4] [--which scipy,gpu] [--variants ...]
 """
 import argparse
 import json
@@ -10,7 +10,7 @@ import os
 import sys
 import time
 
-sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__)))))
 import numpy as np  # noqa: E402
 import scipy.sparse.linalg as spla  # noqa: E402
 
