@@ -1304,6 +1304,10 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     for (int j = 0; j < b; j++) xdev = std::max(xdev, std::fabs(hN[2 * j + 1] - 1.0));
     force_full = !(xdev <= c->xdev_tol);
     for (int j = 0; j < b; j++) res[j] = std::sqrt(hN[2 * j]) / std::sqrt(hN[2 * j + 1]);
+    for (int j = 0; j < b; j++)
+      if (!std::isfinite(res[j]))
+        return set_err(PC_ENUMERIC, "pc_bands: non-finite residual at iteration " + std::to_string(it) +
+                                        " (column " + std::to_string(j) + ")");
     if (c->tail_guard > 0 && c->w_guard >= 0 && !ug_ok && !tail_on) {
       // the slowest wanted columns converge at a rate set by their gap to the guard Ritz values; the
       // guard columns that never get W stay poor (Res ~ 1e1), so in the tail the first tail_guard of

@@ -367,7 +367,9 @@ int launch_update_tmap(const UtBlocks& blk, const cplx* C, int ldc, int r, const
       for (int j = 0; j < blk.nc[k]; j++) mp.crow[col + j] = blk.crow[k][j];
     }
     col += (blk.nc[k] + PC_UT_ALIGN - 1) / PC_UT_ALIGN * PC_UT_ALIGN;
-    if (k == 0) mp.split = col;
+    // the X block ends on a DMMA k-step (4 columns): phase 1 runs k over [split, pe) for P' and phase 2
+    // over [0, split) for X C_X, so no k-step may straddle the split (W and P may start at any even column)
+    if (k == 0) mp.split = col = (col + 3) & ~3;
   }
   mp.pe = std::max((col + 3) & ~3, 4);
   if (mp.pe > 80 || r > 32) return -1;

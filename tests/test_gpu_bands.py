@@ -222,7 +222,9 @@ def test_bands_warm_start_path_continuation(api):
                                   {"update_compact": 1}, {"trim_locked": 0}, {"sticky_lock": 1},
                                   {"update_stream": 1}, {"gram_derive": 1}, {"update_tmap": 1},
                                   {"update_tmap": 0}, {"gram_tmap": 0}, {"gram_tmap": 1, "sticky_lock": 1},
-                                  {"precond": 1}, {"precond": 1, "trim_locked": 0}, {"tail_guard": 3, "tail_at": 5}])
+                                  {"precond": 1}, {"precond": 1, "trim_locked": 0}, {"tail_guard": 3, "tail_at": 5},
+                                  {"guard": 1}, {"guard": 2}, {"guard": 3}, {"guard": 4}, {"guard": 5}, {"guard": 7},
+                                  {"guard": 8}, {"guard": 3, "precond": 1}, {"guard": 7, "update_tmap": 0}])
 def test_bands_option_variants(api, opts):
     """Alternative LOBPCG kernel paths (fused update + next Gram, unfused residual, bulk-copy update
     tiles, full Gram every iteration) reach the same eigenvalues as the dense oracle."""
@@ -243,3 +245,20 @@ def test_bands_option_variants(api, opts):
     assert r["status"][0] == 0
     op = O.PenalizedOperator(n, k, A, e, masks)
     assert rel(r["omega2"][0], O.eigs_dense(op, 10)) <= 1e-8
+
+
+@pytest.mark.parametrize("guard", [4, 5, 6])
+def test_bands_nev20_block_sizes(api, guard):
+    """C5's band count (nev = 20, b = nev + guard = 24-26, the library maximum) at n = 8 against the dense oracle: every
+    block width maps onto the TMA update stage layout (the X block ends on a DMMA k-step)."""
+    A = synth.lattice("fcc")
+    n = 8
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("fcc_diamond", A, n)
+    k = np.array([PI, PI, PI])
+    ctx = api.pc_create(A, n, e, masks)
+    api.pc_set_option(ctx, "guard", guard)
+    r = api.pc_bands(ctx, [k], nev=20, tol=TOL)
+    assert r["status"][0] == 0
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    assert rel(r["omega2"][0], O.eigs_dense(op, 20)) <= 1e-8
