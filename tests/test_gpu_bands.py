@@ -262,3 +262,21 @@ def test_bands_nev20_block_sizes(api, guard):
     assert r["status"][0] == 0
     op = O.PenalizedOperator(n, k, A, e, masks)
     assert rel(r["omega2"][0], O.eigs_dense(op, 20)) <= 1e-8
+
+
+@pytest.mark.parametrize("nev", [1, 2, 3, 5, 7, 12, 16])
+@pytest.mark.parametrize("precond", [0, 1])
+def test_bands_nev_sweep(api, nev, precond):
+    """Band counts 1-16 (block widths 7-22 with the default guard) with both preconditioners against
+    the dense oracle (FCC diamond, pseudochiral, n = 8, a generic k)."""
+    A = synth.lattice("fcc")
+    n = 8
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("fcc_diamond", A, n)
+    k = np.array([0.3, -1.1, 2.0])
+    ctx = api.pc_create(A, n, e, masks)
+    api.pc_set_option(ctx, "precond", precond)
+    r = api.pc_bands(ctx, [k], nev=nev, tol=TOL)
+    assert r["status"][0] == 0
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    assert rel(r["omega2"][0], O.eigs_dense(op, nev)) <= 1e-8
