@@ -186,8 +186,10 @@ PRECOND_DESC = {"kp": "K_P^{-1}, the paper's FFT-diagonal preconditioner (PAPER.
 
 
 def workload_config(W, args):
+    eps_desc = {"pc13": "pseudochiral eps_lat=13 beta=0.875, PAPER.md:1083-1093",
+                "iso13": "isotropic eps_lat=13, PAPER.md:1082", "vacuum": "vacuum"}.get(W.eps, W.eps)
     return {"workload": f"{W.name}: {W.lattice.upper()} lattice, {W.geometry} inclusion, eps1={W.eps} "
-                        f"(pseudochiral eps_lat=13 beta=0.875, PAPER.md:1083-1093), n={W.n}, {W.nev} bands, "
+                        f"({eps_desc}), n={W.n}, {W.nev} bands, "
                         f"tol={args.tol:g}, k-path {len(W.kpoints())} points",
             "n": W.n, "nev": W.nev, "block": W.nev + (args.guard if args.guard is not None else 6), "tol": args.tol, "lattice": W.lattice,
             "geometry": W.geometry, "eps_mode": "crossdof",
