@@ -197,6 +197,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "precond"      0 (default): LOBPCG and pc_precond use the paper's K_P^{-1};
  *                  1: the eps-weighted preconditioner (see pc_precond; beyond the paper): one extra
  *                  5-pass apply of the active W columns per iteration, ~40 % fewer iterations
+ *   "precond_fuse" 1 (default): with precond = 1, pc_bands runs the preconditioner's last pass and the
+ *                  next apply's first pass as one pass; 0: separately
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
  *                  Diagonal/Trivial mode); 0: 7-pass pipeline with the standalone stencil
  *   "plane_fuse"   1: at n = 128 the y-inverse, x-inverse + M_eps + x-forward and y-forward passes of

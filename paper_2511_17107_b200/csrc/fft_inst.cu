@@ -33,6 +33,7 @@ cudaError_t PC_CAT(fft_launch_, PC_FFT_N)(int axis, int dir, int kind, const Col
                                           const ColPtrs& xh, int ncols, const PassArgs& a, cudaStream_t st) {
   if (kind == 1) return run_one<2, +1, OP_KAH, 3>(in, out, xh, ncols, a, st);
   if (kind == 2) return run_one<2, -1, OP_KAG, 3>(in, out, xh, ncols, a, st);
+  if (kind == 3) return run_one<2, -1, OP_KAGH, 3>(in, out, xh, ncols, a, st);
   if (dir < 0) {
     if (axis == 0) return run_one<0, -1, OP_NONE, 1>(in, out, xh, ncols, a, st);
     if (axis == 1) return run_one<1, -1, OP_NONE, 1>(in, out, xh, ncols, a, st);

@@ -15,12 +15,18 @@
 // OP_KAG   (epilogue): y = kappa x s + conj(kappa) g  = K_A s + gamma K_B xhat
 //          with g read back from xh.p[col] (one complex per mode instead of re-reading the 3 components
 //          of xhat: 32 B per point per column of HBM traffic instead of 48)
+// OP_KAGH  (eps-weighted preconditioner + apply, DESIGN R16): the last pass of the preconditioner and the
+//          first pass of the following apply on its output, in one HBM round trip per tile: forward z-DFT,
+//          W = (kappa x s + conj(kappa) g) / |kappa|^2 (stored to out), then u = scale (W x conj(kappa)) and
+//          g' = gamma2 (kappa . W) (g' over g in xh.p[col]), inverse z-DFT of u stored to xh.p[OUT2 + col].
 // with kappa_i(m) = sum_a ktab[(3 i + a) N + m_a]  (Dhat_i symbols, reading R3).
 #pragma once
+#include <type_traits>
 #include "kernels.h"
 #include "dft.cuh"
 
-enum { OP_NONE = 0, OP_KAH = 1, OP_KAG = 2 };
+enum { OP_NONE = 0, OP_KAH = 1, OP_KAG = 2, OP_KAGH = 3 };
+constexpr int OP_KAGH_OUT2 = 96;  // OP_KAGH: xh.p[OP_KAGH_OUT2 + col] = second output column (ncols <= 96)
 
 template <int N>
 struct FftPlan;
@@ -224,40 +230,77 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
       __syncthreads();
     }
 
-    // ---- step A: R2 DFTs of size R1 (stride R2) + twiddle W_N^{j2 k1}; in place
-    for (int i = tid; i < C * TP * R2; i += NT) {
-      int p = i % TP, j2 = (i / TP) % R2, c = i / (TP * R2);
-      cplx v[R1];
+    // ---- steps A + B (two-step Stockham, in place in the tile)
+    auto dft = [&](auto dirc) {
+      constexpr int D = decltype(dirc)::value;
+      // step A: R2 DFTs of size R1 (stride R2) + twiddle W_N^{j2 k1}; in place
+      for (int i = tid; i < C * TP * R2; i += NT) {
+        int p = i % TP, j2 = (i / TP) % R2, c = i / (TP * R2);
+        cplx v[R1];
 #pragma unroll
-      for (int j1 = 0; j1 < R1; j1++) v[j1] = s[SI(c, j2 + R2 * j1, p)];
-      Dft<R1, DIR>::run(v);
+        for (int j1 = 0; j1 < R1; j1++) v[j1] = s[SI(c, j2 + R2 * j1, p)];
+        Dft<R1, D>::run(v);
 #pragma unroll
-      for (int k1 = 0; k1 < R1; k1++) {
-        cplx w = tw[(j2 * k1) % N];
-        if (DIR > 0) w.y = -w.y;
-        s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+        for (int k1 = 0; k1 < R1; k1++) {
+          cplx w = tw[(j2 * k1) % N];
+          if (D > 0) w.y = -w.y;
+          s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+        }
       }
-    }
-    __syncthreads();
-
-    // ---- step B: R1 DFTs of size R2 (contiguous blocks) -> natural order k1 + R1 k2
-    {
-      const int p = tid % TP, k1 = tid / TP;  // NT = TP * R1: one item per thread per component
+      __syncthreads();
+      // step B: R1 DFTs of size R2 (contiguous blocks) -> natural order k1 + R1 k2
+      {
+        const int p = tid % TP, k1 = tid / TP;  // NT = TP * R1: one item per thread per component
 #pragma unroll 1
-      for (int c = 0; c < C; c++) {
-        cplx v[R2];
+        for (int c = 0; c < C; c++) {
+          cplx v[R2];
 #pragma unroll
-        for (int j2 = 0; j2 < R2; j2++) v[j2] = s[SI(c, R2 * k1 + j2, p)];
-        Dft<R2, DIR>::run(v);
-        __syncthreads();
+          for (int j2 = 0; j2 < R2; j2++) v[j2] = s[SI(c, R2 * k1 + j2, p)];
+          Dft<R2, D>::run(v);
+          __syncthreads();
 #pragma unroll
-        for (int k2 = 0; k2 < R2; k2++) s[SI(c, k1 + R1 * k2, p)] = v[k2];
+          for (int k2 = 0; k2 < R2; k2++) s[SI(c, k1 + R1 * k2, p)] = v[k2];
+        }
       }
-    }
-    __syncthreads();
+      __syncthreads();
+    };
+    dft(std::integral_constant<int, DIR>{});
 
     // ---- store (with fused epilogue)
-    if constexpr (OP == OP_KAG) {
+    if constexpr (OP == OP_KAGH) {
+      cplx* gkx = const_cast<cplx*>(xh.p[col]);
+      cplx* gout2 = const_cast<cplx*>(xh.p[OP_KAGH_OUT2 + col]);
+      const int p = tid % TP;
+      cplx g[EPT];
+#pragma unroll
+      for (int q = 0; q < EPT; q++) g[q] = ldg(gkx + tm.off(tid / TP + q * (NT / TP), p));
+#pragma unroll
+      for (int q = 0; q < EPT; q++) {
+        const int j = tid / TP + q * (NT / TP);
+        const int o = tm.off(j, p);
+        const cplx k1 = kxy[0] + ktz[j], k2 = kxy[1] + ktz[N + j], k3 = kxy[2] + ktz[2 * N + j];
+        const cplx s1 = s[SI(0, j, p)], s2 = s[SI(1, j, p)], s3 = s[SI(2, j, p)];
+        const double kk = k1.x * k1.x + k1.y * k1.y + k2.x * k2.x + k2.y * k2.y + k3.x * k3.x + k3.y * k3.y;
+        const double inv = (kk > a.thr) ? 1.0 / kk : 0.0;
+        const cplx w1 = inv * (cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), g[q]));
+        const cplx w2 = inv * (cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), g[q]));
+        const cplx w3 = inv * (cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), g[q]));
+        gout[o] = w1;
+        gout[N3 + o] = w2;
+        gout[2 * N3 + o] = w3;
+        // first pass of the apply on W: u = scale (W x conj kappa), g' = gamma2 (kappa . W)
+        gkx[o] = a.gamma2 * (cmul(k1, w1) + cmul(k2, w2) + cmul(k3, w3));
+        s[SI(0, j, p)] = a.scale * (cmul(w2, conjg(k3)) - cmul(w3, conjg(k2)));
+        s[SI(1, j, p)] = a.scale * (cmul(w3, conjg(k1)) - cmul(w1, conjg(k3)));
+        s[SI(2, j, p)] = a.scale * (cmul(w1, conjg(k2)) - cmul(w2, conjg(k1)));
+      }
+      __syncthreads();
+      dft(std::integral_constant<int, +1>{});
+      for (int e = tid; e < C * N * TP; e += NT) {
+        const int p2 = e % TP, j = (e / TP) % N, c = e / (TP * N);
+        gout2[(long long)c * N3 + tm.off(j, p2)] = s[SI(c, j, p2)];
+      }
+    } else if constexpr (OP == OP_KAG) {
       // same element ownership as the prologue; x_hat (the apply input) and the z-pieces of kappa are
       // loaded for all EPT elements first so the global latencies overlap
       const cplx* gkx = xh.p[col];

@@ -29,6 +29,7 @@ struct PassArgsH {
   double gamma;
   double scale;
   int z0 = 0, nz = 0;  // x/y passes: restrict to z-planes [z0, z0+nz) (nz = 0: all)
+  double gamma2 = 0.0; // OP_KAGH: gamma of the apply that follows the preconditioner
   int kscale = 0;      // OP_KAG: output scaled by 1/|kappa|^2 per mode (0 where |kappa|^2 <= thr): the
   double thr = 0.0;    // last pass of the eps-weighted preconditioner (pcband.cu, precond_eps)
 };

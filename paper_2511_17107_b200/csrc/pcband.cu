@@ -152,6 +152,7 @@ struct pc_ctx {
   int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane.cu; measured slower)
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int precond = 0;             // 0: K_P^{-1}; 1: eps-weighted K_P^{-1} (beyond the paper, see precond_eps)
+  int precond_fuse = 1;        // precond = 1 in pc_bands: its last pass and the apply's first pass as one (OP_KAGH)
   EpsCoef ec_inv{};            // diagonal of M_eps inverted: 1/eps_ii - 1 on the masks I_i (precond = 1)
   int tail_guard = 0;          // > 0: once at most tail_at wanted columns are unconverged, this many more
   int tail_at = 3;             //      guard columns (after nev + w_guard) also get W (see solve_k)
@@ -481,6 +482,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "w_guard") c->w_guard = (int)v;
   else if (k == "tail_guard") c->tail_guard = (int)v;
   else if (k == "precond") c->precond = (int)v;
+  else if (k == "precond_fuse") c->precond_fuse = (int)v;
   else if (k == "tail_at") c->tail_at = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
@@ -562,6 +564,8 @@ static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
 // ------------------------------------------------------------------------------------------
 // apply
 // ------------------------------------------------------------------------------------------
+constexpr int OP_KAGH_OUT2_HOST = 96;  // = OP_KAGH_OUT2 in fft_pass.cuh (second output slots of xh)
+
 // The operator the apply pipeline runs: Op = K_A M K_A^H + gamma K_B (the paper's), or, for
 // the eps-weighted preconditioner, (1/|kappa|^2) (K_A D^{-1} K_A^H + K_B) with D = diag(M_eps) (precond_eps).
 struct ApplyOp {
@@ -573,7 +577,7 @@ static ApplyOp paper_op(const pc_ctx* c) { return ApplyOp{c->eps_mode, &c->ec, 0
 
 static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
                     const ColPtrs& xh, int nc, double scale, cudaStream_t st, int z0 = 0, int nz = 0,
-                    int prec = 0) {
+                    int prec = 0, double gamma2 = 0.0) {
   PassArgsH a;
   a.tw = c->d_tw;
   a.ktab = c->d_ktab;
@@ -583,6 +587,7 @@ static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, c
   a.nz = nz;
   a.kscale = (prec && kind == 2) ? 1 : 0;
   a.thr = c->cur_thr;
+  a.gamma2 = gamma2;
   cudaError_t e = launch_fft_pass(c->n, axis, dir, kind, in, out, xh, nc, a, st);
   if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("fft pass: ") + cudaGetErrorString(e));
   return PC_OK;
@@ -712,6 +717,58 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
 static int precond_eps(pc_ctx* c, const MutColPtrs& W, const MutColPtrs& WS, int nc, cudaStream_t st) {
   const ApplyOp op{PC_EPS_DIAGONAL, &c->ec_inv, 1};
   return apply_fourier(c, to_const(W, nc), W, WS, nc, st, &op);
+}
+
+// W <- T W (W = K_P^{-1} R on entry, see precond_eps) and AW = Op W in 9 passes instead of 10: the
+// preconditioner's last pass and the apply's first pass run as one OP_KAGH pass.  Only for the 5-pass
+// pipeline of z-plane-local media (else: returns 1 and the caller runs the two steps).
+static int precond_apply_fused(pc_ctx* c, const MutColPtrs& W, const MutColPtrs& AW, const MutColPtrs& WS, int nc,
+                               cudaStream_t st) {
+  const bool plane_local = c->fuse_xex && (c->eps_mode != PC_EPS_CROSSDOF || (!c->ec.has[1] && !c->ec.has[2]));
+  if (!plane_local || c->plane_fuse || c->chunk_mb > 0 || nc > OP_KAGH_OUT2_HOST) return 1;
+  const int n = c->n;
+  const double inv_n3 = 1.0 / ((double)n * n * n);
+  const size_t kxb = (size_t)nc * c->n3 * sizeof(cplx);
+  if (kxb > c->kxws.bytes) {
+    cudaStreamSynchronize(st);
+    CHK(c->kxws.ensure(kxb));
+  }
+  ColPtrs KX, none{};
+  for (int j = 0; j < nc; j++) KX.p[j] = c->kxws.as<cplx>() + (size_t)j * c->n3;
+  const ColPtrs Wc = to_const(W, nc), AWc = to_const(AW, nc), WSc = to_const(WS, nc);
+  const double pts = (double)c->n3 * nc;
+  const double fl = 15.0 * std::log2((double)n) * pts;
+  {
+    Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 38.0 * pts, 112.0 * pts);
+    CHK(fft_pass(c, 2, +1, 1, Wc, AW, KX, nc, inv_n3, st, 0, 0, 1));
+  }
+  auto middle = [&](int mode, const EpsCoef& ec) -> int {
+    {
+      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+      CHK(fft_pass(c, 1, +1, 0, AWc, AW, none, nc, 1.0, st));
+    }
+    {
+      Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 100.0 * pts, 96.0 * pts);
+      cudaError_t e = launch_xex(n, mode, AWc, WS, nc, c->d_mask, ec, c->d_tw, 1.0, 0, 0, st);
+      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
+    }
+    Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+    return fft_pass(c, 1, -1, 0, WSc, WS, none, nc, 1.0, st);
+  };
+  CHK(middle(PC_EPS_DIAGONAL, c->ec_inv));
+  {
+    // W = (K_A s + K_B W0)/|kappa|^2 -> W; u = K_A^H W / N^3 -> AW (scratch); g = gamma kappa.W -> KX
+    ColPtrs X2 = KX;
+    for (int j = 0; j < nc; j++) X2.p[OP_KAGH_OUT2_HOST + j] = AW.p[j];
+    Prof p(c, PC_STAT_FFT_Z_KA, st, 1, 2 * fl + 80.0 * pts, 192.0 * pts);
+    CHK(fft_pass(c, 2, -1, 3, WSc, W, X2, nc, inv_n3, st, 0, 0, 1, c->cur_gamma));
+  }
+  CHK(middle(c->eps_mode, c->ec));
+  {
+    Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
+    CHK(fft_pass(c, 2, -1, 2, WSc, AW, KX, nc, 1.0, st));
+  }
+  return PC_OK;
 }
 
 // unitary 3-D DFT per component; dir = -1: F3^H (to Fourier), +1: F3 (to real).  Y may equal X.
@@ -1358,8 +1415,19 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       for (int j : miss) hasW[j] = 1;
     }
     const int nP = (int)actP.size();
-    if (c->precond == 1) CHK(precond_list(WW, act));
-    CHK(apply_list(WW, AWW, act));
+    int pa = 1;  // 0: W preconditioned and AW applied by the fused 9-pass sequence
+    if (c->precond == 1 && c->precond_fuse) {
+      MutColPtrs y, ay, w;
+      mcols(WW, act, y, 0);
+      mcols(AWW, act, ay, 0);
+      for (size_t t = 0; t < act.size(); t++) w.p[t] = wsp.p[t];
+      pa = precond_apply_fused(c, y, ay, w, na, st);
+      if (pa < 0) return pa;
+    }
+    if (pa) {
+      if (c->precond == 1) CHK(precond_list(WW, act));
+      CHK(apply_list(WW, AWW, act));
+    }
     int p = 0;
     cplx* const dG0 = dG;  // the previous step's Gram (read by the derived assembly)
     dG = (dG == dGbuf[0]) ? dGbuf[1] : dGbuf[0];

@@ -223,6 +223,7 @@ def test_bands_warm_start_path_continuation(api):
                                   {"update_stream": 1}, {"gram_derive": 1}, {"update_tmap": 1},
                                   {"update_tmap": 0}, {"gram_tmap": 0}, {"gram_tmap": 1, "sticky_lock": 1},
                                   {"precond": 1}, {"precond": 1, "trim_locked": 0}, {"tail_guard": 3, "tail_at": 5},
+                                  {"precond": 1, "precond_fuse": 0}, {"precond": 1, "fuse_xex": 0},
                                   {"guard": 1}, {"guard": 2}, {"guard": 3}, {"guard": 4}, {"guard": 5}, {"guard": 7},
                                   {"guard": 8}, {"guard": 3, "precond": 1}, {"guard": 7, "update_tmap": 0}])
 def test_bands_option_variants(api, opts):
