@@ -197,6 +197,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "precond"      0 (default): LOBPCG and pc_precond use the paper's K_P^{-1};
  *                  1: the eps-weighted preconditioner (see pc_precond; beyond the paper): one extra
  *                  5-pass apply of the active W columns per iteration, ~40 % fewer iterations
+ *   "xex_ring"     1: ring variant of the fused x-pass (each row read once; measured slower);
+ *                  0 (default) (process-wide knob)
  *   "precond_fuse" 1 (default): with precond = 1, pc_bands runs the preconditioner's last pass and the
  *                  next apply's first pass as one pass; 0: separately
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or

@@ -58,6 +58,19 @@ static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, 
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
+  if (xex_ring()) {  // ring variant: one CTA per (z-plane, strip of SH rows)
+    using RC = XrCfg<N>;
+    auto rk = xexr_kernel<N, MODE>;
+    static bool rattr = false;
+    if (!rattr) {
+      cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RC::SMEM);
+      if (e != cudaSuccess) return e;
+      rattr = true;
+    }
+    dim3 rgrid(RC::STRIPS * (nz > 0 ? nz : N), ncols);
+    rk<<<rgrid, RC::NT, RC::SMEM, st>>>(in, out, mask, ec, tw, scale, nz > 0 ? z0 : 0);
+    return cudaGetLastError();
+  }
   dim3 grid((N / Cfg::TP) * (nz > 0 ? nz : N), ncols);
   kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale, nz > 0 ? z0 : 0);
   return cudaGetLastError();

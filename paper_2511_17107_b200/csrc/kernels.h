@@ -38,6 +38,9 @@ struct PassArgsH {
 // (148 SMs x resident CTAs per SM), so that kernels of concurrent k-point solves (other streams)
 // can co-reside (process-wide tuning knob, pc_set_option "grid_frac"; default 1).
 void set_grid_frac(double f);
+// Fused x-pass variant (process-wide knob, pc_set_option "xex_ring"): 1 = ring kernel (xexr_kernel).
+void set_xex_ring(int v);
+int xex_ring();
 int grid_cap(int ctas_per_sm);
 
 // FFT passes ------------------------------------------------------------------------------

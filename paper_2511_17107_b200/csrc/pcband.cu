@@ -483,6 +483,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "tail_guard") c->tail_guard = (int)v;
   else if (k == "precond") c->precond = (int)v;
   else if (k == "precond_fuse") c->precond_fuse = (int)v;
+  else if (k == "xex_ring") set_xex_ring((int)v);
   else if (k == "tail_at") c->tail_at = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
   else if (k == "fuse_gram") c->fuse_gram = (int)v;
