@@ -464,7 +464,10 @@ def main():
     # bands.solve_concurrent (host k in, host omega^2 / Res out), contexts destroyed -- all timed.
     e2e = None
     if args.e2e_steps > 0:
-        pin = torch.from_numpy(masks.reshape(-1)).pin_memory()
+        # the timed contexts are done: free them first (at C5 one context holds ~94 GB of the 180)
+        for c_ in ctxs:
+            c_.close()
+        pin =torch.from_numpy(masks.reshape(-1)).pin_memory()
         pinned_masks = pin.numpy().reshape(masks.shape)
         nctx = len(ctxs)
 

@@ -30,7 +30,21 @@
 #include "tma.cuh"
 
 constexpr int UT_SEG = 16;              // modes per tile
-constexpr int UT_THREADS = 128;         // warp w: modes [8 (w & 1), +8), n-tiles {w >> 1, +2, ...}
+// Warp w: modes [8 (w & 1), +8), n-tiles {w >> 1, + UtGeom<NT>::NG, ...}.  NG = 2 n-tile groups (4 warps)
+// for b <= 16; for b > 16 one group per 8-column n-tile (6 warps at 168 registers, 2 CTAs/SM, for
+// b = 17..24; 8 warps, 1 CTA/SM, for b = 25..32), so a warp holds one output tile (2 tiles per warp needed
+// 255 registers with spills).  Measured: b = 22 5.82 -> 4.66 ms at n = 128, b = 26
+// 31.2 -> 27.0 ms at n = 192.  PC_UT_NG2: the 4-warp layout for every b.
+template <int NT>
+struct UtGeom {
+#ifdef PC_UT_NG2
+  static constexpr int NG = 2;
+#else
+  static constexpr int NG = (NT <= 2) ? 2 : NT;
+#endif
+  static constexpr int THREADS = 64 * NG;
+  static constexpr int NTW = (NT + NG - 1) / NG;  // n-tiles per warp
+};
 #ifndef PC_UT_STAGES
 #define PC_UT_STAGES 2
 #endif
@@ -84,15 +98,15 @@ struct UtOut {
 };
 
 template <int NT>
-__global__ void __launch_bounds__(UT_THREADS, (NT <= 2) ? PC_UT_MINB : 1) update_tmap_kernel(
+__global__ void __launch_bounds__(UtGeom<NT>::THREADS, (NT <= 2) ? PC_UT_MINB : ((NT == 3 && UtGeom<NT>::NG == 3) ? 2 : 1)) update_tmap_kernel(
     const __grid_constant__ UtMaps mp, const cplx* __restrict__ C, int ldc, int r, const __grid_constant__ UtOut yo,
     const double* __restrict__ lam, int n, const cplx* __restrict__ kt, double gamma, double thr, int deflate0,
     double* partial) {
-  constexpr int NTW = (NT + 1) / 2;
+  constexpr int NTW = UtGeom<NT>::NTW, NG = UtGeom<NT>::NG, UT_THREADS = UtGeom<NT>::THREADS;
   extern __shared__ __align__(1024) unsigned char utsm_raw[];
   // dynamic shared memory is only guaranteed 16-B aligned: round the ring up to 1024 B
   cplx* Ring = reinterpret_cast<cplx*>((reinterpret_cast<uintptr_t>(utsm_raw) + 1023) & ~(uintptr_t)1023);
-  __shared__ double red[4][NTW][4][2][2];
+  __shared__ double red[2 * NG][NTW][4][2][2];
   __shared__ __align__(8) unsigned long long full[UT_STAGES];
   const int n3 = n * n * n;
   const int pe = mp.pe, split = mp.split;
@@ -168,7 +182,7 @@ __global__ void __launch_bounds__(UT_THREADS, (NT <= 2) ? PC_UT_MINB : 1) update
       for (int s = 0; s < 3; s++) a[s] = Sc[ut_idx(mm, s, lrow)];
 #pragma unroll
       for (int i = 0; i < NTW; i++) {
-        const int nt = ng + 2 * i;
+        const int nt = ng + NG * i;
         if (nt >= NT) break;
         const cplx cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
         const double cs = cv.x + cv.y;
@@ -197,7 +211,7 @@ __global__ void __launch_bounds__(UT_THREADS, (NT <= 2) ? PC_UT_MINB : 1) update
     auto store = [&](int o, bool keep) {
 #pragma unroll
       for (int i = 0; i < NTW; i++) {
-        const int nt = ng + 2 * i;
+        const int nt = ng + NG * i;
         if (nt >= NT) break;
 #pragma unroll
         for (int e = 0; e < 2; e++) {
@@ -242,7 +256,7 @@ __global__ void __launch_bounds__(UT_THREADS, (NT <= 2) ? PC_UT_MINB : 1) update
       const bool zero0 = deflate0 && mi == 0;
 #pragma unroll
       for (int i = 0; i < NTW; i++) {
-        const int nt = ng + 2 * i;
+        const int nt = ng + NG * i;
         if (nt >= NT) break;
 #pragma unroll
         for (int e = 0; e < 2; e++) {
@@ -292,7 +306,7 @@ __global__ void __launch_bounds__(UT_THREADS, (NT <= 2) ? PC_UT_MINB : 1) update
     }
   __syncthreads();
   for (int c = tid; c < r; c += UT_THREADS) {
-    const int nt = c / 8, i = nt >> 1, g = nt & 1;
+    const int nt = c / 8, i = nt / NG, g = nt % NG;
     const int ln = (c % 8) / 2, e = c % 2;
     double a = 0, b = 0;
     for (int q = 0; q < 2; q++) {  // the two row-group warps of n-tile group g, fixed order
@@ -338,6 +352,7 @@ static int run_update_tmap(const UtMaps& mp, const cplx* C, int ldc, int r, cons
     attr = true;
   }
   int occ = 0;
+  constexpr int UT_THREADS = UtGeom<NT>::THREADS;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, UT_THREADS, smem);
   occ = std::max(1, std::min(8, occ));
   const long long n3 = (long long)n * n * n;
