@@ -371,12 +371,13 @@ def eigs_dense(op: PenalizedOperator, nev: int) -> np.ndarray:
 
 
 def eigs_iterative(op: PenalizedOperator, nev: int, tol: float = 1e-8, seed: int = 0,
-                   maxiter: int = 2000, guard: int = 5):
+                   maxiter: int = 2000, guard: int = 5, info: dict | None = None):
     """The nev smallest eigenvalues of the penalised operator by SciPy's LOBPCG (library
     primitive) in Fourier coordinates with the oracle's own K_P^{-1} as
     preconditioner.  At k = 0 the null space (constant fields; in Fourier
     coordinates the three zero-mode unit vectors) is passed as a constraint (reading R12).
-    Returns (eigenvalues, residual norms ||Op x - w x|| per P:1059-1062)."""
+    Returns (eigenvalues, residual norms ||Op x - w x|| per P:1059-1062).  If ``info`` is a
+    dict, the number of LOBPCG iterations SciPy ran is stored in info["iterations"]."""
     n = op.n
     dim = op.dim
     gamma = op.gamma
@@ -404,7 +405,12 @@ def eigs_iterative(op: PenalizedOperator, nev: int, tol: float = 1e-8, seed: int
         for c in range(3):
             Y[c * n ** 3, c] = 1.0
         X0[[0, n ** 3, 2 * n ** 3], :] = 0.0
-    w, V = spla.lobpcg(Aop, X0, M=Mop, Y=Y, tol=tol, maxiter=maxiter, largest=False)
+    if info is None:
+        w, V = spla.lobpcg(Aop, X0, M=Mop, Y=Y, tol=tol, maxiter=maxiter, largest=False)
+    else:
+        w, V, hist = spla.lobpcg(Aop, X0, M=Mop, Y=Y, tol=tol, maxiter=maxiter, largest=False,
+                                 retResidualNormsHistory=True)
+        info["iterations"] = len(hist)
     order = np.argsort(w)
     w, V = w[order], V[:, order]
     R = mv(V) - V * w[None, :]
