@@ -324,15 +324,71 @@ def test_trivial_lambda_min_bound_P755(seed):
 
 
 def test_S_norm_le_1_P791():
+    """Prop 3.5: ||S_ij|| <= 1, on the S_ij blocks of the oracle's own M_CrossDoF
+    (eps_ij = 1 off the diagonal makes the (i,j) block equal to S_ij)."""
     n = 4
     masks = synth.make_masks("random", np.eye(3), n, seed=9)
-    T = O.transfer_T(n)
-    I = [np.diag(masks[c].reshape(-1).astype(float)) for c in range(3)]
-    for (i, j), Tij in zip([(0, 1), (0, 2), (1, 2)], T):
-        S = 0.5 * (I[i] @ Tij.toarray() + Tij.toarray() @ I[j])
+    M = O.permittivity_matrix(np.ones((3, 3), complex), masks, "crossdof").toarray()
+    N3 = n ** 3
+    for i, j in [(0, 1), (0, 2), (1, 2)]:
+        S = M[i * N3:(i + 1) * N3, j * N3:(j + 1) * N3]
+        assert abs(S).max() > 0
         assert np.linalg.norm(S, 2) <= 1 + 1e-12
         for p in (1, np.inf):
             assert np.linalg.norm(S, p) <= 1 + 1e-12
+
+
+def _dof_positions(n):
+    """DoF locations in units of h, 0-based index (a,b,c) = (x,y,z) (reading R6):
+    E1 at (a+1/2, b+1, c+1), E2 at (a+1, b+1/2, c+1), E3 at (a+1, b+1, c+1/2).  Row order of
+    a component block: flat index (c*n + b)*n + a (x fastest)."""
+    c, b, a = np.meshgrid(np.arange(n), np.arange(n), np.arange(n), indexing="ij")
+    base = np.stack([a.ravel(), b.ravel(), c.ravel()], axis=1).astype(float) + 1.0
+    return [base - np.array(off) for off in ((0.5, 0, 0), (0, 0.5, 0), (0, 0, 0.5))]
+
+
+@pytest.mark.parametrize("mode", ["diagonal", "trivial", "crossdof"])
+@pytest.mark.parametrize("n", [4, 5])
+def test_permittivity_entrywise_from_dof_geometry_P607_P664(mode, n):
+    """M_eps built entry by entry from the DoF-level definitions, on random masks where I1, I2,
+    I3 and I_V all differ, compared EXACTLY with the oracle:
+      M_ii(p,p) = (eps_ii - 1) I_i[p] + 1                       (P:610-613);
+      Trivial:  M_ij(p,p) = eps_ij I_V[p], M_ji = conj            (P:635);
+      CrossDoF: M_ij(p,q) = eps_ij (I_i[p] + I_j[q]) / 8 for the four E^j DoFs q nearest to the
+                E^i DoF p (|dx_i| = |dx_j| = h/2 on the two axes of i, j, same coordinate on the
+                third: the interpolation of P:640-654), M_ji(q,p) = conj(eps_ij)(I_i[p]+I_j[q])/8
+                (S_ij = (I_i T_ij + T_ij I_j)/2)."""
+    rng = np.random.default_rng(100 + n)
+    masks = (rng.random((4, n, n, n)) < 0.5).astype(np.uint8)
+    assert all((masks[a] != masks[b]).any() for a in range(4) for b in range(a))
+    e = synth.eps_sdd() if mode != "diagonal" else np.diag([0.3, 0.55, 0.8]).astype(complex)
+    N3 = n ** 3
+    I = [masks[c].reshape(-1).astype(float) for c in range(4)]
+    ref = np.zeros((3 * N3, 3 * N3), complex)
+    for i in range(3):
+        for p in range(N3):
+            ref[i * N3 + p, i * N3 + p] = (e[i, i].real - 1.0) * I[i][p] + 1.0
+    pos = _dof_positions(n)
+    for i, j in [(0, 1), (0, 2), (1, 2)]:
+        if mode == "trivial":
+            for p in range(N3):
+                ref[i * N3 + p, j * N3 + p] = e[i, j] * I[3][p]
+                ref[j * N3 + p, i * N3 + p] = np.conj(e[i, j]) * I[3][p]
+        elif mode == "crossdof":
+            third = 3 - i - j
+            for p in range(N3):
+                d = pos[j] - pos[i][p]
+                d = d - n * np.round(d / n)            # periodic minimum image
+                near = (np.abs(np.abs(d[:, i]) - 0.5) < 1e-12) & (np.abs(np.abs(d[:, j]) - 0.5) < 1e-12) \
+                    & (np.abs(d[:, third]) < 1e-12)
+                qs = np.nonzero(near)[0]
+                assert qs.size == 4
+                for q in qs:
+                    w = (I[i][p] + I[j][q]) / 8.0
+                    ref[i * N3 + p, j * N3 + q] = e[i, j] * w
+                    ref[j * N3 + q, i * N3 + p] = np.conj(e[i, j]) * w
+    M = O.permittivity_matrix(e, masks, mode).toarray()
+    assert np.array_equal(M, ref)
 
 
 def test_permittivity_special_cases():
