@@ -134,7 +134,7 @@ int pc_fft3(pc_ctx *ctx, const void *X, void *Y, int ncols, long long ld, int di
  * (kernel-compensation formulation P:254-262; LOBPCG with soft locking P:1055-1056).
  *   kpts     host, nk*3 Cartesian Bloch vectors.
  *   nev      number of eigenvalues (>= 1); block size = nev + guard (pc_set_option "guard",
- *            default 5, reading R14).
+ *            default 6, reading R14).
  *   tol      convergence when Res_j = ||Op x_j - w_j x_j|| / ||x_j|| <= tol for all j < nev
  *            (the paper uses 1e-5).
  *   maxit    iteration cap (SPEC default 500).
@@ -177,12 +177,6 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  its residual rises above tol again
  *   "gram_refresh" every n-th iteration forms the full Gram matrices instead of using
  *                  X^H X = I, X^H A X = Lambda (default 16; 0 = never)
- *   "gram_derive"  1: the X^H P, P^H P, X^H A P, P^H A P blocks of the Rayleigh-Ritz Gram come from
- *                  the previous step's Gram and Ritz coefficients (P = S0 C0P), so only S^H [W AW] is
- *                  formed from the vectors (15 % less Gram time at n=128, but numerically unstable
- *                  near convergence on degenerate spectra); 0 (default): S^H [W P AW AP] from the vectors
- *   "derive_tau"   cancellation factor sum|C0P||G0||C0P| / |P^H (.) P| above which a derived Gram is
- *                  rejected and formed from the vectors instead (default 1e5)
  *   "xdev_tol"     if max_j | |X_j|^2 - 1 | exceeds this, the next Gram is formed in full from the
  *                  vectors (default 1e-10)
  *   "p_restart"    1 (default): drop the P block when the basis is numerically rank deficient
@@ -192,13 +186,9 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  paper); 0 (default): cold start.  Setting the option forgets the stored block.
  *   "w_guard"      guard columns that receive a search direction W (default 0: only the nev
  *                  wanted columns; -1: all b columns)
- *   "tail_guard"   > 0: once at most "tail_at" (default 3) wanted columns are unconverged, this many
- *                  more guard columns receive W (default 0; measured: no fewer iterations)
  *   "precond"      0 (default): LOBPCG and pc_precond use the paper's K_P^{-1};
  *                  1: the eps-weighted preconditioner (see pc_precond; beyond the paper): one extra
  *                  5-pass apply of the active W columns per iteration, ~40 % fewer iterations
- *   "xex_ring"     1: ring variant of the fused x-pass (each row read once; measured slower);
- *                  0 (default) (process-wide knob)
  *   "precond_fuse" 1 (default): with precond = 1, pc_bands runs the preconditioner's last pass and the
  *                  next apply's first pass as one pass; 0: separately
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
@@ -209,17 +199,10 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  per 15 columns); 0 (default): the three passes
  *   "fuse_resid"   1 (default): both block updates + next residual + K_P^{-1} in one pass; 0: two
  *                  update launches and a separate residual pass
- *   "chunk_mb"     > 0: run the middle FFT passes in z-slabs of about this many MB (default 0: off)
- *   "update_warps" 4 (default), 8 or 16 warps per block-update CTA (process-wide tuning knob)
- *   "gram_tmap"    1: Gram S^H [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu, S and T
- *                  share one shared-memory buffer; measured slower); 0 (default): cp.async chunks (gram.cu)
  *   "update_tmap"  1 (default): block-update kernel with TMA tensor-copy row tiles in a 2-stage
  *                  ring (update_tmap.cu); 0: per-thread cp.async tiles (update_all.cu)
- *   "gram_ks"      2 (default) or 1 warp groups splitting each Gram row chunk (process-wide knob)
  *   "jacobi_tol"   rotation threshold of the Rayleigh-Ritz Jacobi sweeps, |a_pq| <= tol sqrt(|a_pp a_qq|)
  *                  (process-wide; default 1e-16)
- *   "grid_frac"    (0, 1]: persistent block-update and Gram grids cover this fraction of the GPU's
- *                  resident-CTA slots, leaving room for concurrent solves (process-wide; default 1)
  */
 int pc_set_option(pc_ctx *ctx, const char *key, double value);
 

@@ -41,112 +41,6 @@ void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx*
   gram_assemble_kernel<<<(2 * p * p + 255) / 256, 256, 0, st>>>(Gp, lam, b, c, G);
 }
 
-// [G_M | G_A] of S = [X W P] with the P blocks derived from the previous Rayleigh-Ritz step instead
-// of formed from the vectors.  The previous basis S0 (p0 columns, X0 first) had the Gram G0 =
-// [G0_M | G0_A] and Ritz coefficients C0 (p0 x b); the update made X = S0 C0 and P = S0 C0P, where
-// C0P is C0 with its X0 rows zeroed (the recurrence of block LOBPCG).  Hence
-//   X^H P = C0^H G0_M C0P,  P^H P = C0P^H G0_M C0P,  and the same with G0_A for A:
-// exact in exact arithmetic, so only S^H [W AW] (Gw, p x 2na) has to be formed from the vectors.
-// X^H X = I, X^H A X = Lambda as in gram_assemble_kernel; W^H P = (P^H W)^H etc. by Hermitian
-// symmetry.  One CTA; p0, p <= 80.
-constexpr int GD_MAX = 80;
-__global__ void __launch_bounds__(256) gram_derive_kernel(const cplx* __restrict__ G0, int p0,
-                                                          const cplx* __restrict__ C0, const int* __restrict__ actP,
-                                                          int nP, const cplx* __restrict__ Gw, int na,
-                                                          const double* __restrict__ lam, int b, cplx* G,
-                                                          double* cancel) {
-  extern __shared__ __align__(16) double gdsm[];
-  __shared__ double cmax[256];
-  const int tid = threadIdx.x;
-  const int p = b + na + nP, bp = b + nP;
-  cplx* Ms = reinterpret_cast<cplx*>(gdsm);  // [2][nP][p0]: G0_{M,A}[:, b:p0] C0[b:p0, actP]
-  cplx* Ds = Ms + 2 * nP * p0;               // [2][nP][b+nP]: rows < b: X^H (.) P, rows >= b: P^H (.) P
-  auto M = [&](int h, int i, int t) -> cplx& { return Ms[((size_t)h * nP + t) * p0 + i]; };
-  auto D = [&](int h, int u, int t) -> cplx& { return Ds[((size_t)h * nP + t) * bp + u]; };
-  for (int e = tid; e < 2 * p0 * nP; e += blockDim.x) {
-    const int h = e / (p0 * nP), r = e % (p0 * nP);
-    const int i = r % p0, t = r / p0;
-    const cplx* g = G0 + (size_t)h * p0 * p0;
-    const int ct = actP[t];
-    cplx acc = mk(0, 0);
-    for (int s = b; s < p0; s++) acc = acc + cmul(g[(size_t)s * p0 + i], C0[(size_t)ct * p0 + s]);
-    M(h, i, t) = acc;
-  }
-  __syncthreads();
-  for (int e = tid; e < 2 * (b + nP) * nP; e += blockDim.x) {
-    const int h = e / ((b + nP) * nP), r = e % ((b + nP) * nP);
-    const int u = r % (b + nP), t = r / (b + nP);
-    const int cu = (u < b) ? u : actP[u - b];
-    const int s0 = (u < b) ? 0 : b;  // C0P has no X0 rows
-    cplx acc = mk(0, 0);
-    for (int s = s0; s < p0; s++) acc = acc + cmul(conjg(C0[(size_t)cu * p0 + s]), M(h, s, t));
-    D(h, u, t) = acc;
-  }
-  __syncthreads();
-  // cancellation in P = S0 C0P: sum |C0P| |G0| |C0P| against P^H (.) P per column and both Grams.  The
-  // derived entries carry absolute errors ~ eps * that sum, so a large ratio means they are unreliable
-  // (the host then forms this Gram from the vectors).
-  double cm = 0.0;
-  for (int e = tid; e < 2 * nP; e += blockDim.x) {
-    const int h = e / nP, t = e % nP;
-    const cplx* g = G0 + (size_t)h * p0 * p0;
-    const int ct = actP[t];
-    double bound = 0.0;
-    for (int r = b; r < p0; r++) {
-      const double cr = sqrt(abs2(C0[(size_t)ct * p0 + r]));
-      double row = 0.0;
-      for (int q = b; q < p0; q++) row += sqrt(abs2(g[(size_t)q * p0 + r])) * sqrt(abs2(C0[(size_t)ct * p0 + q]));
-      bound += cr * row;
-    }
-    const double d = fabs(D(h, b + t, t).x);
-    cm = fmax(cm, d > 0.0 ? bound / d : 1e300);
-  }
-  cmax[tid] = cm;
-  __syncthreads();
-  if (tid == 0) {
-    double m = 0.0;
-    for (int i = 0; i < blockDim.x; i++) m = fmax(m, cmax[i]);
-    *cancel = m;
-  }
-  const int bw = b + na;
-  for (int e = tid; e < 2 * p * p; e += blockDim.x) {
-    const int h = e / (p * p), r = e % (p * p);
-    int i = r % p, j = r / p;
-    const bool lower = i > j;
-    if (lower) {  // Hermitian: G[i][j] = conj(G[j][i])
-      const int t = i;
-      i = j;
-      j = t;
-    }
-    cplx v;
-    if (j < b) {
-      v = (i == j) ? mk(h ? lam[i] : 1.0, 0.0) : mk(0, 0);
-    } else if (j < bw) {
-      v = Gw[(size_t)(h * na + (j - b)) * p + i];      // S^H W, S^H AW: formed from the vectors
-    } else if (i < b) {
-      v = D(h, i, j - bw);                              // X^H P (derived)
-    } else if (i < bw) {
-      v = conjg(Gw[(size_t)(h * na + (i - b)) * p + j]);  // W^H P = (P^H W)^H
-    } else {
-      v = D(h, b + (i - bw), j - bw);                   // P^H P (derived)
-    }
-    G[(size_t)h * p * p + r] = lower ? conjg(v) : v;
-  }
-}
-
-int launch_gram_derive(const cplx* G0, int p0, const cplx* C0, const int* actP, int nP, const cplx* Gw, int na,
-                       const double* lam, int b, cplx* G, double* cancel, cudaStream_t st) {
-  if (p0 > GD_MAX || nP < 1 || b + na + nP > GD_MAX) return -1;
-  const size_t smem = (size_t)2 * nP * (p0 + b + nP) * sizeof(cplx);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(gram_derive_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
-    attr = true;
-  }
-  gram_derive_kernel<<<1, 256, smem, st>>>(G0, p0, C0, actP, nP, Gw, na, lam, b, G, cancel);
-  return 0;
-}
-
 // ------------------------------------------------------------------------------------------
 // Update: phase 1  acc = sum_{m in [split, p)} S[:, m] C[m, :]  -> Y1 (optional)
 //         phase 2  acc += sum_{m in [0, split)} S[:, m] C[m, :] -> Y2 (+ Add)
@@ -157,8 +51,6 @@ int launch_gram_derive(const cplx* G0, int p0, const cplx* C0, const int* actP, 
 // MMAs per m8n8k4 step of 4 complex m:  P1 = S_r C_r, P2 = S_i C_i, P3 = (S_r + S_i)(C_r + C_i),
 // Re = P1 - P2, Im = P3 - P1 - P2.
 // ------------------------------------------------------------------------------------------
-static int g_update_warps = 4;  // CTA = g_update_warps x 8 rows (pc_set_option "update_warps": 4, 8, 16)
-void set_update_warps(int w) { g_update_warps = (w == 8 || w == 16) ? w : 4; }
 
 HD int pitch2mod8(int p) {
   int x = p + 1;
@@ -265,11 +157,7 @@ static void run_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, i
   constexpr int U_ROWS = 8 * WARPS;
   const int pe = (p + 3) & ~3, ps = pitch4mod8(pe);
   const size_t smem = (size_t)(2 * pe * (U_ROWS + 2) + NT * 8 * ps) * sizeof(cplx);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(update_kernel<NT, WARPS>, cudaFuncAttributeMaxDynamicSharedMemorySize, 220 * 1024);
-    attr = true;
-  }
+  smem_attr((const void*)update_kernel<NT, WARPS>, 220 * 1024);
   const long long ntiles = (len + U_ROWS - 1) / U_ROWS;
   const int occ = std::max(1, std::min(64 / WARPS, (int)((227 * 1024) / (smem + 1024))));
   const int grid = (int)std::min<long long>(ntiles, 148LL * occ);
@@ -290,7 +178,5 @@ static void launch_update_w(const ColPtrs& S, int p, const cplx* C, int ldc, int
 
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st) {
-  if (g_update_warps == 4) launch_update_w<4>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
-  else if (g_update_warps == 16) launch_update_w<16>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
-  else launch_update_w<8>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
+  launch_update_w<4>(S, p, C, ldc, r, split, Y1, Y2, add, len, st);
 }

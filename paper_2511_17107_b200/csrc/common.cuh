@@ -2,11 +2,29 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <stdint.h>
+#include <mutex>
+#include <set>
+#include <utility>
 
 #define DEV __device__ __forceinline__
 #define HD __host__ __device__ __forceinline__
 
 typedef double2 cplx;
+
+// cudaFuncSetAttribute is a per-device setting: the dynamic shared-memory limit of `kern` is set once
+// per (kernel, current device).  (A process-wide "done" flag would leave the kernel without it on a
+// second device used by another context, and its launches would fail.)
+inline cudaError_t smem_attr(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kern, dev})) return cudaSuccess;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e == cudaSuccess) done.insert({kern, dev});
+  return e;
+}
 
 HD cplx mk(double r, double i) { return make_double2(r, i); }
 HD cplx operator+(cplx a, cplx b) { return mk(a.x + b.x, a.y + b.y); }

@@ -38,10 +38,6 @@ cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& i
   }
 }
 
-static int g_xex_ring = 0;
-void set_xex_ring(int v) { g_xex_ring = v; }
-int xex_ring() { return g_xex_ring; }
-
 cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                        const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st) {
   switch (n) {

@@ -14,10 +14,10 @@ static cudaError_t run_one(const ColPtrs& in, const MutColPtrs& out, const ColPt
   constexpr int N = PC_FFT_N;
   using Cfg = TileCfg<N, C>;
   auto kern = fft_pass_kernel<N, AXIS, DIR, OP, C>;
+  cudaError_t e = smem_attr((const void*)kern, (int)Cfg::SMEM);
+  if (e != cudaSuccess) return e;
   static int occ = 0;
   if (!occ) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(kern, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, Cfg::NT, Cfg::SMEM);
     if (occ < 1) occ = 1;
@@ -52,25 +52,8 @@ static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, 
   constexpr int N = PC_FFT_N;
   using Cfg = XexCfg<N>;
   auto kern = xex_kernel<N, MODE>;
-  static bool attr_done = false;
-  if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
-    if (e != cudaSuccess) return e;
-    attr_done = true;
-  }
-  if (xex_ring()) {  // ring variant: one CTA per (z-plane, strip of SH rows)
-    using RC = XrCfg<N>;
-    auto rk = xexr_kernel<N, MODE>;
-    static bool rattr = false;
-    if (!rattr) {
-      cudaError_t e = cudaFuncSetAttribute(rk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)RC::SMEM);
-      if (e != cudaSuccess) return e;
-      rattr = true;
-    }
-    dim3 rgrid(RC::STRIPS * (nz > 0 ? nz : N), ncols);
-    rk<<<rgrid, RC::NT, RC::SMEM, st>>>(in, out, mask, ec, tw, scale, nz > 0 ? z0 : 0);
-    return cudaGetLastError();
-  }
+  cudaError_t e = smem_attr((const void*)kern, (int)Cfg::SMEM);
+  if (e != cudaSuccess) return e;
   dim3 grid((N / Cfg::TP) * (nz > 0 ? nz : N), ncols);
   kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale, nz > 0 ? z0 : 0);
   return cudaGetLastError();

@@ -20,8 +20,7 @@ struct GramCfg {
 
 template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS>
 __global__ void __launch_bounds__(GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>::THREADS)
-gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_per_split, int nmb, cplx* partial,
-            int hb, int hc) {
+gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_per_split, int nmb, cplx* partial) {
   using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
   constexpr int BM = Cfg::BM, BN = Cfg::BN, NTH = Cfg::THREADS, PITCH = Cfg::PITCH;
   extern __shared__ __align__(16) double gsm[];
@@ -69,26 +68,6 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
 
   // warp tiles entirely outside [0, p) x [0, q) skip their MMAs (warp-uniform)
   const bool live = (m0 + wm * WM * 8 < p) && (n0 + wn * WN * 8 < q);
-  // Hermitian blocks (hb >= 0): S = [X Y] with |X| = hb, T = [Y AY] with |Y| = hc.  Entries (m, n) with
-  // m - hb > n' (n' = n or n - hc) are the strict lower triangles of Y^H Y and Y^H A Y: 8x8 tiles made
-  // only of such entries (or padding) are not computed; launch_gram_assemble mirrors them.
-  unsigned skip = 0u;
-  if (hb >= 0) {
-#pragma unroll
-    for (int mt = 0; mt < WM; mt++)
-#pragma unroll
-      for (int nt = 0; nt < WN; nt++) {
-        const int tm0 = m0 + wm * WM * 8 + mt * 8, tn0 = n0 + wn * WN * 8 + nt * 8;
-        bool all = true;
-        for (int e = 0; e < 64 && all; e++) {
-          const int m = tm0 + e / 8, n = tn0 + e % 8;
-          if (m >= p || n >= q) continue;
-          const int np_ = (n < hc) ? n : n - hc;
-          all = (m >= hb) && (m - hb > np_);
-        }
-        if (all) skip |= 1u << (mt * WN + nt);
-      }
-  }
   const int nchunks = (r1 > r0) ? (int)((r1 - r0 + KC - 1) / KC) : 0;
   // prologue: STAGES-1 chunks in flight (one commit group per chunk, empty groups allowed)
 #pragma unroll
@@ -106,9 +85,6 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
       const int st = ch % STAGES;
       const double* A = As + st * BM * PITCH;
       const double* B = Bs + st * BN * PITCH;
-      // the skip test is warp-uniform and fixed for the launch: two copies of the k-loop keep the
-      // common no-skip path free of branches between the DMMAs
-      auto kloop = [&](auto has_skip) {
 #pragma unroll 2
         for (int s4 = kg; s4 < KC / 4; s4 += KS) {
           const int kk = 2 * (4 * s4 + (lane & 3));  // complex row 4 s4 + (lane & 3), interleaved doubles
@@ -133,17 +109,11 @@ gram_kernel(ColPtrs S, int p, ColPtrs T, int q, long long len, long long rows_pe
           for (int mt = 0; mt < WM; mt++)
 #pragma unroll
             for (int nt = 0; nt < WN; nt++) {
-              if constexpr (decltype(has_skip)::value) {
-                if (skip & (1u << (mt * WN + nt))) continue;
-              }
               dmma(p1[mt][nt][0], p1[mt][nt][1], ar[mt], br[nt]);
               dmma(p2[mt][nt][0], p2[mt][nt][1], ai[mt], bi[nt]);
               dmma(p3[mt][nt][0], p3[mt][nt][1], ad[mt], bs[nt]);
             }
         }
-      };
-      if (skip) kloop(std::true_type{});
-      else kloop(std::false_type{});
     }
     __syncthreads();  // the stage consumed here is refilled STAGES-1 iterations later
   }
@@ -220,24 +190,19 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
 #ifndef PC_GRAM40_ST
 #define PC_GRAM40_ST 4
 #endif
-static double g_grid_frac = 1.0;
-void set_grid_frac(double f) { g_grid_frac = (f > 0.0 && f <= 1.0) ? f : 1.0; }
-int grid_cap(int ctas_per_sm) { return std::max(1, (int)(g_grid_frac * 148.0 * ctas_per_sm + 0.5)); }
-
-static int g_gram_ks = 2;  // pc_set_option "gram_ks" (1 or 2), process-wide tuning knob
-void set_gram_ks(int k) { g_gram_ks = (k == 1) ? 1 : 2; }
+int grid_cap(int ctas_per_sm) { return std::max(1, 148 * ctas_per_sm); }
 
 size_t gram_partial_bytes(int p, int q) { return (size_t)4 * 148 * p * q * sizeof(cplx) + 4096; }
 
 template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS = 1>
 static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
-                     int hb, int hc, cudaStream_t st) {
+                     cudaStream_t st) {
   using Cfg = GramCfg<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
   static_assert(KS == 1 || (size_t)WARPS_M * WARPS_N * 32 * WM * WN * 6 * 8 <= Cfg::SMEM, "reduction buffer");
   auto kern = gram_kernel<WM, WN, WARPS_M, WARPS_N, KC, STAGES, KS>;
+  smem_attr((const void*)kern, (int)Cfg::SMEM);
   static int ctas_per_sm = 0;
   if (!ctas_per_sm) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::SMEM);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ctas_per_sm, kern, Cfg::THREADS, Cfg::SMEM);
     ctas_per_sm = std::max(1, ctas_per_sm);
   }
@@ -249,7 +214,7 @@ static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long
   long long rps = (len + ns - 1) / ns;
   rps = (rps + KC - 1) / KC * KC;
   ns = (int)((len + rps - 1) / rps);
-  kern<<<dim3(nblk, ns), Cfg::THREADS, Cfg::SMEM, st>>>(S, p, T, q, len, rps, nmb, partial, hb, hc);
+  kern<<<dim3(nblk, ns), Cfg::THREADS, Cfg::SMEM, st>>>(S, p, T, q, len, rps, nmb, partial);
   const int pq = p * q;
   gram_reduce_kernel<<<(pq + 255) / 256, 256, 0, st>>>(partial, ns, pq, G);
 }
@@ -257,7 +222,7 @@ static void run_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long
 // Block shape: least padded output area (the DMMA pipe is the bound, padding is wasted MMAs), ties
 // broken towards fewer CTA blocks per output.
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
-                 cudaStream_t st, int hb, int hc) {
+                 cudaStream_t st) {
   struct Opt { int bm, bn; };
   const Opt opts[] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}, {40, 40}, {40, 64}, {64, 64}, {80, 64},
                       {80, 96}, {24, 32}, {48, 96}, {40, 24}};
@@ -272,15 +237,15 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
   }
   // KS = 2 (two warp groups per chunk, accumulators folded at the end) where the fold buffer fits
 #define PC_GRAM_CASE(WM_, WN_, WAM, WAN, KC_, ST_)                                          \
-  if (g_gram_ks == 2 && WM_ * WN_ <= 6 &&                                \
+  if (WM_ * WN_ <= 6 &&                                                                      \
       (size_t)WAM * WAN * 32 * WM_ * WN_ * 48 <=                                            \
                             GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM)                  \
     run_gram<WM_, WN_, WAM, WAN, KC_, ST_, (WM_ * WN_ <= 6 &&             \
                                             WAM * WAN * 32 * WM_ * WN_ * 48 <=               \
                                             (int)GramCfg<WM_, WN_, WAM, WAN, KC_, ST_, 2>::SMEM) ? 2 : 1>( \
-        S, p, T, q, len, G, partial, hb, hc, st);                                           \
+        S, p, T, q, len, G, partial, st);                                           \
   else                                                                                      \
-    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, 1>(S, p, T, q, len, G, partial, hb, hc, st);
+    run_gram<WM_, WN_, WAM, WAN, KC_, ST_, 1>(S, p, T, q, len, G, partial, st);
   switch (best) {
     case 0: PC_GRAM_CASE(3, 2, 2, 4, 16, 3) break;
     case 1: PC_GRAM_CASE(3, 2, 2, 3, 16, 3) break;

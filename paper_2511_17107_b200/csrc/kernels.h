@@ -34,13 +34,7 @@ struct PassArgsH {
   double thr = 0.0;    // last pass of the eps-weighted preconditioner (pcband.cu, precond_eps)
 };
 
-// Persistent-grid share: the block-update and Gram kernels size their grids to this fraction of
-// (148 SMs x resident CTAs per SM), so that kernels of concurrent k-point solves (other streams)
-// can co-reside (process-wide tuning knob, pc_set_option "grid_frac"; default 1).
-void set_grid_frac(double f);
-// Fused x-pass variant (process-wide knob, pc_set_option "xex_ring"): 1 = ring kernel (xexr_kernel).
-void set_xex_ring(int v);
-int xex_ring();
+// Persistent grids: 148 SMs x resident CTAs per SM.
 int grid_cap(int ctas_per_sm);
 
 // FFT passes ------------------------------------------------------------------------------
@@ -89,41 +83,14 @@ void launch_pw_scatter(const MutColPtrs& X, const PwEntry* e, int ne, int n3, cu
 // dense block algebra ------------------------------------------------------------------------
 // G (p x q, column-major, ld p) = S^H T over rows [0, len): S p columns, T q columns.
 size_t gram_partial_bytes(int p, int q);
-void set_gram_ks(int k);  // tuning knob: 1 or 2 warp groups per Gram chunk
 // [G_M | G_A] (p x 2p) from Gp = S^H [W P AW AP] (p x 2c), S = [X W P], b = |X|, c = |W| + |P|,
 // assuming X^H X = I, X^H A X = diag(lambda) (Ritz vectors of the previous Rayleigh-Ritz step).
 void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);
-// [G_M | G_A] (p x 2p, p = b + na + nP) of S = [X W_a P_a] from Gw = S^H [W_a AW_a] (p x 2na, ld p) and
-// the P blocks derived from the previous step: G0 (p0 x 2p0, the Gram its Rayleigh-Ritz used), C0
-// (p0 x b, ld p0, its Ritz coefficients), actP (device, nP ints) = the P columns kept.  *cancel (device)
-// = max over P columns and both Grams of sum|C0P||G0||C0P| / |P^H (.) P| (the cancellation factor of
-// the derived entries).  Returns -1 if the sizes are out of range (nothing launched).
-int launch_gram_derive(const cplx* G0, int p0, const cplx* C0, const int* actP, int nP, const cplx* Gw, int na,
-                       const double* lam, int b, cplx* G, double* cancel, cudaStream_t st);
-// hb >= 0: S = [X Y] (|X| = hb), T = [Y AY] (|Y| = hc) with Y^H Y, Y^H A Y Hermitian: 8x8 tiles of their
-// strict lower triangles are skipped (left unwritten in G; launch_gram_assemble mirrors them).
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
-                 cudaStream_t st, int hb = -1, int hc = 0);
-// Gp = S^H T for S = [X W P], T = [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu).  Block k
-// (0 X, 1 W, 2 P, 3 AW, 4 AP) = box columns [c0[k], c0[k] + nc[k]) of a slot (base[k] = its column 0,
-// slot_cols[k] columns, stride ld); lidx[k][j] (k < 3) / tidx[k][j] (k >= 1) = row of Gp / column of
-// Gp of box column j (-1: not in the basis).  Gp is p x q column-major (p, q from the maps), written
-// by a fixed-order reduction of the CTA partials in `partial` (>= gram_tmap_partial_bytes()).
-// Returns -1 (nothing launched) if the shape is not supported (S > 40 or T > 40 columns).
-struct GtBlocks {
-  const cplx* base[5];
-  int slot_cols[5];
-  long long ld;
-  int c0[5], nc[5];
-  signed char lidx[5][32], tidx[5][32];
-};
-size_t gram_tmap_partial_bytes();
-int launch_gram_tmap(const GtBlocks& blk, long long len, cplx* G, cplx* partial, cudaStream_t st);
-
+                 cudaStream_t st);
 // Block update (r <= 32 output columns, C column-major ld = ldc):
 //   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr; columns with Y1->p[c] == nullptr skipped)
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])
-void set_update_warps(int w);  // tuning knob (4, 8 or 16 warps per update CTA)
 void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int split, const MutColPtrs* Y1,
                    const MutColPtrs& Y2, const ColPtrs* add, long long len, cudaStream_t st);
 
@@ -132,13 +99,6 @@ void launch_update(const ColPtrs& S, int p, const cplx* C, int ldc, int r, int s
 // R = AX' - X' diag(lam), W[:, c] = K_P^{-1} R[:, c] for W.p[c] != nullptr (mode 0 zeroed if deflate0),
 // per-CTA |R_c|^2, |X'_c|^2 into partial[(c * grid + cta) * 2 + {0,1}].  r <= 32.  Returns the grid
 // (<= max_grid) for launch_reduce_partial.
-// Same contract as launch_update_all, barrier-free streaming kernel (update_stream.cu).
-int launch_update_stream(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
-                         const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
-                         const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
-                         int deflate0, double* partial, int max_grid, cudaStream_t st);
-void set_update_tma(int v);
-void set_update_compact(int v);  // tuning knob: 1 = update kernel without a shared copy of C (4 CTAs/SM)  // tuning knob: 1 = bulk-copy (TMA) row tiles, 0 = per-thread cp.async
 int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                       const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
@@ -162,24 +122,6 @@ int launch_update_tmap(const UtBlocks& blk, const cplx* C, int ldc, int r, const
                        const MutColPtrs& Y2s, const MutColPtrs& Y1a, const MutColPtrs& Y2a, const MutColPtrs& W,
                        const double* lam, int n, const cplx* kt, double gamma, double thr, int deflate0,
                        double* partial, int max_grid, cudaStream_t st);
-
-// Update + residual + K_P^{-1} + the next iteration's Gram blocks in one pass (update_gram.cu):
-// S = [X W P] (p columns, X first: split = b), outputs X', AX' (b columns), P', AP', W' (nw columns,
-// null pointers skipped), norm partials as launch_update_all, and the reduced Gram tiles in gred
-// (G1 = [X' W' P']^H [W' P' AP'], G2 = (AX')^H W' in 8x8 tiles).  Requires update_gram_supported().
-// Returns the grid (for launch_reduce_partial).
-bool update_gram_supported(int p, int b, int nw);
-struct UgFlops { double flops_per_row; };  // algorithmic Gram flops of the fused pass per row (8 per complex MAC)
-inline UgFlops ug_flops(int b, int nw) { return {8.0 * ((double)(b + 2 * nw) * 3 * nw + (double)b * nw)}; }
-size_t update_gram_partial_bytes(int b, int nw);
-int launch_update_gram(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int b, int nw,
-                       const MutColPtrs& Xo, const MutColPtrs& Po, const MutColPtrs& AXo, const MutColPtrs& APo,
-                       const MutColPtrs& Wo, const double* lam, int n, const cplx* kt, double gamma, double thr,
-                       int deflate0, double* npart, cplx* gpart, cplx* gred, int max_grid, cudaStream_t st);
-// [G_M | G_A] (p x 2p) of S = [X W_a P_a] from gred, Gww = W_a^H A W_a (na x na), lambda; act (device,
-// na ints) = the active columns among the nw W'/P' columns.
-void launch_ug_assemble(const cplx* red, int b, int nw, const int* act, int na, int haveP, const cplx* Gww,
-                        const double* lam, int p, cplx* G, cudaStream_t st);
 
 // Rayleigh-Ritz ------------------------------------------------------------------------------
 // G = [G_M | G_A] (p x 2p, column-major ld p).  Outputs C (p x nb, ld p), lambda (nb), info[0] = rank,

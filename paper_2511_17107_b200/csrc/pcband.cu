@@ -154,20 +154,10 @@ struct pc_ctx {
   int precond = 0;             // 0: K_P^{-1}; 1: eps-weighted K_P^{-1} (beyond the paper, see precond_eps)
   int precond_fuse = 1;        // precond = 1 in pc_bands: its last pass and the apply's first pass as one (OP_KAGH)
   EpsCoef ec_inv{};            // diagonal of M_eps inverted: 1/eps_ii - 1 on the masks I_i (precond = 1)
-  int tail_guard = 0;          // > 0: once at most tail_at wanted columns are unconverged, this many more
-  int tail_at = 3;             //      guard columns (after nev + w_guard) also get W (see solve_k)
   int fuse_resid = 1;          // both block updates + residual + K_P^{-1} in one pass (update_all.cu)
-  int update_stream = 0;       // 1: barrier-free streaming update kernel (update_stream.cu)
-  int gram_tmap = 0;           // 1: Gram S^H [W P AW AP] with TMA tensor-copy row chunks (gram_tmap.cu; slower)
   int update_tmap = 1;         // 1: update kernel with TMA tensor-copy row tiles (update_tmap.cu); 0: cp.async tiles
   int trim_locked = 1;         // W', P', AP' only for the columns active in this iteration (see solve_k)
-  int gram_derive = 0;         // 1: P blocks of the Gram from the previous Gram and Ritz coefficients (see solve_k; unstable)
-  double derive_tau = 1e5;     // ... unless their cancellation factor exceeds this (then from the vectors)
   double xdev_tol = 1e-10;     // max | |X_j|^2 - 1 | above which the next Gram is formed in full
-  int derive_fallbacks = 0;    // iterations of the last solve whose derived Gram was rejected
-  int gram_herm = 0;           // 1: skip the strict lower triangles of the Hermitian Gram blocks (measured slower: warp imbalance)
-  int fuse_gram = 0;           // 1: ... and the next iteration's Gram blocks in the same pass (update_gram.cu; measured slower)
-  double chunk_mb = 0.0;       // > 0: L2-chunked middle apply passes of about this many MB per buffer
   int start_mode = 1;          // 0: Gaussian start block; 1: transverse plane waves of the lowest |kappa|^2
   int start_precond = 1;       // plane-wave start: Gaussian admixture through K_P^{-1} (see solve_k)
 #ifndef PC_START_NOISE
@@ -180,7 +170,7 @@ struct pc_ctx {
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
-  DevBuf lob, small, gpart, ugbuf, cbuf;
+  DevBuf lob, small, gpart, cbuf;
   double* h_pinned = nullptr;
   cudaStream_t stream = nullptr;
   // profiling
@@ -424,7 +414,6 @@ extern "C" void pc_destroy(pc_ctx* c) {
   auto t2 = now();
   c->ws.release();
   c->kxws.release();
-  c->ugbuf.release();
   c->lob.release();
   c->small.release();
   c->gpart.release();
@@ -480,28 +469,13 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "fuse_xex") c->fuse_xex = (int)v;
   else if (k == "plane_fuse") c->plane_fuse = (int)v;
   else if (k == "w_guard") c->w_guard = (int)v;
-  else if (k == "tail_guard") c->tail_guard = (int)v;
   else if (k == "precond") c->precond = (int)v;
   else if (k == "precond_fuse") c->precond_fuse = (int)v;
-  else if (k == "xex_ring") set_xex_ring((int)v);
-  else if (k == "tail_at") c->tail_at = (int)v;
   else if (k == "fuse_resid") c->fuse_resid = (int)v;
-  else if (k == "fuse_gram") c->fuse_gram = (int)v;
-  else if (k == "gram_herm") c->gram_herm = (int)v;
   else if (k == "trim_locked") c->trim_locked = (int)v;
-  else if (k == "gram_derive") c->gram_derive = (int)v;
-  else if (k == "derive_tau") c->derive_tau = v;
   else if (k == "xdev_tol") c->xdev_tol = v;
-  else if (k == "update_stream") c->update_stream = (int)v;
   else if (k == "update_tmap") c->update_tmap = (int)v;
-  else if (k == "gram_tmap") c->gram_tmap = (int)v;
-  else if (k == "update_warps") set_update_warps((int)v);
-  else if (k == "gram_ks") set_gram_ks((int)v);
-  else if (k == "grid_frac") set_grid_frac(v);
   else if (k == "jacobi_tol") set_jacobi_tol(v);
-  else if (k == "update_tma") set_update_tma((int)v);
-  else if (k == "update_compact") set_update_compact((int)v);
-  else if (k == "chunk_mb") c->chunk_mb = v;
   else if (k == "start_noise") c->start_noise = v;
   else if (k == "start_precond") c->start_precond = (int)v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
@@ -627,57 +601,26 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
   const bool plane_local = c->fuse_xex && (op.mode != PC_EPS_CROSSDOF || (!op.ec->has[1] && !op.ec->has[2]));
   if (plane_local) {
-    // Middle passes (y-inverse, x-inverse + M_eps + x-forward, y-forward) in L2-sized chunks of
-    // (column, z-planes): the chunk written by one pass is re-read by the next while it is still in
-    // the 126 MB L2, so HBM only sees the first read of u and the final write-back of s.
-    // A chunk is a slab of z-planes of ALL nc columns (so each launch still fills the GPU), sized so
-    // that the slab (chunk_mb per buffer) stays in L2 between the three passes.
-    const double chunk_bytes = c->chunk_mb * 1048576.0;
-    const double plane_bytes = 3.0 * n * n * sizeof(cplx) * nc;  // one z-plane, 3 components, nc columns
-    int nzc = n;
-    if (c->chunk_mb > 0) {
-      nzc = (int)std::max(1.0, std::floor(chunk_bytes / plane_bytes));
-      while (nzc < n && n % nzc) nzc--;  // divisor of n
-      nzc = std::min(nzc, n);
-    }
-    if (c->plane_fuse && c->chunk_mb <= 0 && plane_supported(n)) {
+    if (c->plane_fuse && plane_supported(n)) {
       // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane.cu)
-      const double cp = (double)nc * n * n * n;
-      const double cfl = 15.0 * std::log2((double)n) * cp;
-      Prof p(c, PC_STAT_EPS, st, 1, 4 * cfl + 100.0 * cp, 97.0 * cp);
+      Prof p(c, PC_STAT_EPS, st, 1, 4 * fl + 100.0 * pts, 97.0 * pts);
       cudaError_t e = launch_plane(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
       if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("plane pass: ") + cudaGetErrorString(e));
     } else {
-    const int ccols = nc;
-    for (int j0 = 0; j0 < nc; j0 += ccols) {
-      const int cn = std::min(ccols, nc - j0);
-      ColPtrs Ys, Ws;
-      MutColPtrs Ym, Wm;
-      for (int j = 0; j < cn; j++) {
-        Ys.p[j] = Yc.p[j0 + j];
-        Ws.p[j] = Wc.p[j0 + j];
-        Ym.p[j] = Y.p[j0 + j];
-        Wm.p[j] = WS.p[j0 + j];
+      // y-inverse, (x-inverse + M_eps + x-forward) fused, y-forward
+      {
+        Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+        CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
       }
-      for (int z0 = 0; z0 < n; z0 += nzc) {
-        const int nz = (nzc == n) ? 0 : nzc;
-        const double cp = (double)cn * n * n * (nz ? nz : n);
-        const double cfl = 15.0 * std::log2((double)n) * cp;
-        {
-          Prof p(c, PC_STAT_FFT_MID, st, 1, cfl, 96.0 * cp);
-          CHK(fft_pass(c, 1, +1, 0, Ys, Ym, none, cn, 1.0, st, z0, nz));
-        }
-        {
-          Prof p(c, PC_STAT_EPS, st, 1, 2 * cfl + 100.0 * cp, 96.0 * cp);
-          cudaError_t e = launch_xex(n, op.mode, Ys, Wm, cn, c->d_mask, *op.ec, c->d_tw, 1.0, z0, nz, st);
-          if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
-        }
-        {
-          Prof p(c, PC_STAT_FFT_MID, st, 1, cfl, 96.0 * cp);
-          CHK(fft_pass(c, 1, -1, 0, Ws, Wm, none, cn, 1.0, st, z0, nz));
-        }
+      {
+        Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 100.0 * pts, 97.0 * pts);
+        cudaError_t e = launch_xex(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, 1.0, 0, 0, st);
+        if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xex pass: ") + cudaGetErrorString(e));
       }
-    }
+      {
+        Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+        CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
+      }
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
@@ -726,7 +669,7 @@ static int precond_eps(pc_ctx* c, const MutColPtrs& W, const MutColPtrs& WS, int
 static int precond_apply_fused(pc_ctx* c, const MutColPtrs& W, const MutColPtrs& AW, const MutColPtrs& WS, int nc,
                                cudaStream_t st) {
   const bool plane_local = c->fuse_xex && (c->eps_mode != PC_EPS_CROSSDOF || (!c->ec.has[1] && !c->ec.has[2]));
-  if (!plane_local || c->plane_fuse || c->chunk_mb > 0 || nc > OP_KAGH_OUT2_HOST) return 1;
+  if (!plane_local || c->plane_fuse || nc > OP_KAGH_OUT2_HOST) return 1;
   const int n = c->n;
   const double inv_n3 = 1.0 / ((double)n * n * n);
   const size_t kxb = (size_t)nc * c->n3 * sizeof(cplx);
@@ -1046,26 +989,6 @@ extern "C" int pc_bench_block(pc_ctx* c, int which, int b, int na, int nP, int r
                                        dPart, rg, st);
       if (g < 0) return set_err(PC_ECUDA, "pc_bench_block: tensor map encoding failed");
       launch_reduce_partial(dPart, g, b, dLam + 0 * b, st);
-    } else if (which == 4) {
-      GtBlocks gb;
-      memset(&gb, -1, sizeof(gb));
-      gb.ld = len;
-      const int cw = na + nP;
-      const int slots[5] = {0, 8, 4, 9, 5}, cnt[5] = {b, na, nP, na, nP};
-      const int lofs[5] = {0, b, b + na, -1, -1}, tofs[5] = {-1, 0, na, cw, cw + na};
-      for (int kb = 0; kb < 5; kb++) {
-        gb.base[kb] = col(slots[kb], 0);
-        gb.slot_cols[kb] = b;
-        gb.c0[kb] = 0;
-        gb.nc[kb] = cnt[kb];
-        for (int j = 0; j < cnt[kb]; j++) {
-          gb.lidx[kb][j] = (signed char)(lofs[kb] >= 0 ? lofs[kb] + j : -1);
-          gb.tidx[kb][j] = (signed char)(tofs[kb] >= 0 ? tofs[kb] + j : -1);
-        }
-      }
-      if (launch_gram_tmap(gb, len, dGp, c->gpart.as<cplx>(), st) != 0)
-        return set_err(PC_EINVAL, "pc_bench_block: shape not supported by gram_tmap");
-      launch_gram_assemble(dGp, dLam, b, cw, dG, st);
     } else if (which == 1) {
       ColPtrs T;
       const int cw = na + nP;
@@ -1187,47 +1110,25 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   auto col = [&](int slot, int j) { return base + ((size_t)slot * b + j) * len; };
   enum { XA = 0, AXA, XB, AXB, PA, APA, PB, APB, WW, AWW };
   int sX = XA, sAX = AXA, sXn = XB, sAXn = AXB, sP = PA, sAP = APA, sPn = PB, sAPn = APB;
-  // small device buffers: G (maxp x 2maxp), C (maxp x b), lam, info, rr scratch, resid partials, norms
+  // small device buffers: G (maxp x 2maxp), Gp (maxp x 2maxp), C (maxp x b), rr scratch, lam, norms,
+  // residual partials, info
   const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)3 * 80 * 80;
   const int rg = resid_grid(c->n);
-  size_t small_bytes = (3 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2 + 2) * sizeof(double) +
-                       (size_t)(8 + maxp) * sizeof(int) + 64;
+  size_t small_bytes = (2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(b + 2 * b + rg * b * 2) * sizeof(double) +
+                       (size_t)8 * sizeof(int) + 64;
   CHK(c->small.ensure(small_bytes));
   CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
-  // fused update + next-iteration Gram (update_gram.cu): only the first nw columns ever get W and P
+  // only the first nw columns ever get a search direction W (option w_guard; -1: all b)
   const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
-  const bool ug_ok = c->fuse_gram && c->fuse_resid && update_gram_supported(maxp, b, nw);
-  cplx *dUgPart = nullptr, *dUgRed = nullptr, *dGww = nullptr;
-  int* dAct = nullptr;
-  int* hAct = reinterpret_cast<int*>(c->h_pinned + 3072);
-  if (ug_ok) {
-    const size_t pb = update_gram_partial_bytes(b, nw);
-    CHK(c->ugbuf.ensure(pb + (size_t)(48 * 64 + b * b) * sizeof(cplx) + 64 * sizeof(int)));
-    dUgPart = c->ugbuf.as<cplx>();
-    dUgRed = dUgPart + pb / sizeof(cplx);
-    dGww = dUgRed + 48 * 64;
-    dAct = reinterpret_cast<int*>(dGww + b * b);
-  }
-  bool fused_ready = false;  // dUgRed holds the Gram blocks of the current [X W P] (all nw W, P columns)
-  // two Gram buffers: the Rayleigh-Ritz of an iteration reads one, the next iteration's derived P blocks
-  // (option gram_derive) read it while the new Gram is assembled into the other
-  cplx* const dGbuf[2] = {c->small.as<cplx>(), c->small.as<cplx>() + nG};
-  cplx* dG = dGbuf[0];
-  cplx* dGp = dGbuf[1] + nG;
+  cplx* dG = c->small.as<cplx>();
+  cplx* dGp = dG + nG;
   cplx* dC = dGp + nG;
   cplx* dScr = dC + nC;
   double* dLam = reinterpret_cast<double*>(dScr + nScr);
   double* dNorm = dLam + b;
   double* dPart = dNorm + 2 * b;
-  double* dCancel = dPart + (size_t)rg * b * 2;
-  int* dInfo = reinterpret_cast<int*>(dCancel + 2);
-  int* dActP = dInfo + 8;
-  int* hActP = reinterpret_cast<int*>(c->h_pinned + 3584);
-  double* hCancel = c->h_pinned + 3700;
-  double last_cancel = 0.0;
+  int* dInfo = reinterpret_cast<int*>(dPart + (size_t)rg * b * 2);
   bool force_full = false;  // next Gram from the vectors in full (X^H X = I no longer trusted)
-  int p_prev = 0;          // size of the basis of the last Rayleigh-Ritz (dG, dC hold its Gram and C)
-  bool g_prev = false;     // dG / dC describe the basis that produced the current X and P
   double* hN = c->h_pinned;                 // 2b norms
   int* hInfo = reinterpret_cast<int*>(c->h_pinned + 2048);
   MutColPtrs wsp;
@@ -1265,6 +1166,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     }
     cudaMemcpyAsync(hInfo, dInfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, st);
     cudaError_t e = cudaStreamSynchronize(st);
+    // a launch rejected on its configuration is not reported by the synchronisation: check it too
+    if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("rayleigh-ritz: ") + cudaGetErrorString(e));
     return hInfo[0];  // rank
   };
@@ -1330,13 +1233,12 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   std::vector<double> res(b, 0.0);
   c->hist.clear();
   c->hist_b = b;
-  bool haveP = false, resid_ready = false, tail_on = false;
-  c->derive_fallbacks = 0;
+  bool haveP = false, resid_ready = false;
   int it = 0, conv = 0;
   // trim_locked: the update writes W', P', AP' only for the columns that are active in this iteration
   // (soft-locked columns skip 3 column writes each).  A locked column that re-activates (sticky_lock = 0)
   // gets its W from one residual pass and enters without a P column.
-  const bool trim = c->trim_locked && !ug_ok;
+  const bool trim = c->trim_locked != 0;
   std::vector<char> hasW(b, 0), hasP(b, 0);
   for (;; it++) {
     // residuals of every column; W = K_P^{-1} R only for the columns that can receive a search direction
@@ -1354,6 +1256,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     cudaMemcpyAsync(hN, dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
     {
       cudaError_t e = cudaStreamSynchronize(st);
+      if (e == cudaSuccess) e = cudaGetLastError();
       if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("lobpcg: ") + cudaGetErrorString(e));
     }
     if (c->profile) prof_flush(c);
@@ -1366,15 +1269,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (!std::isfinite(res[j]))
         return set_err(PC_ENUMERIC, "pc_bands: non-finite residual at iteration " + std::to_string(it) +
                                         " (column " + std::to_string(j) + ")");
-    if (c->tail_guard > 0 && c->w_guard >= 0 && !ug_ok && !tail_on) {
-      // the slowest wanted columns converge at a rate set by their gap to the guard Ritz values; the
-      // guard columns that never get W stay poor (Res ~ 1e1), so in the tail the first tail_guard of
-      // them get search directions too (cheap then: few wanted columns are still active)
-      int nun = 0;
-      for (int j = 0; j < nev; j++) nun += (res[j] > tol) ? 1 : 0;
-      tail_on = nun <= c->tail_at;
-    }
-    const int wlim = (c->w_guard < 0) ? b : std::min(b, nev + c->w_guard + (tail_on ? c->tail_guard : 0));
+    const int wlim = nw;
     for (int j = 0; j < b; j++) {
       c->hist.push_back(res[j]);
       // soft locking: a converged column leaves the search block (no W, P); with sticky_lock = 0 it
@@ -1386,13 +1281,20 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       if (j < nev && !(res[j] <= tol)) conv = 0;
     }
     if (c->verbose) {
-      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d |X|-1 %.1e cancel %.1e fb %d rr-cycles %d %d %d %d %d res:",
-              kidx, it, rank, hInfo[2], hInfo[1], xdev, last_cancel, c->derive_fallbacks, hInfo[3], hInfo[4],
-              hInfo[5], hInfo[6], hInfo[7]);
+      fprintf(stderr, "[pcband] k%d it %d rank %d chol %d sweeps %d |X|-1 %.1e rr-cycles %d %d %d %d %d res:",
+              kidx, it, rank, hInfo[2], hInfo[1], xdev, hInfo[3], hInfo[4], hInfo[5], hInfo[6], hInfo[7]);
       for (int j = 0; j < b; j++) fprintf(stderr, " %.2e%s", res[j], active[j] ? "" : "*");
       fprintf(stderr, "\n");
     }
-    if (force_full && it < maxit) conv = 0;  // Ritz pairs not trusted: one more step with a full Gram
+    // Ritz pairs not trusted (X^H X drifted from I): one more step with a full Gram, which
+    // re-orthonormalises X, before the convergence test may stop the solve
+    if (force_full && it < maxit) {
+      conv = 0;
+      bool any = false;
+      for (int j = 0; j < wlim; j++) any |= active[j] != 0;
+      if (!any)  // every search column is locked: re-open them for this step (W from one residual pass)
+        for (int j = 0; j < wlim; j++) active[j] = 1;
+    }
     if (conv || it >= maxit) break;
     std::vector<int> act;
     for (int j = 0; j < b; j++)
@@ -1430,9 +1332,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       CHK(apply_list(WW, AWW, act));
     }
     int p = 0;
-    cplx* const dG0 = dG;  // the previous step's Gram (read by the derived assembly)
-    dG = (dG == dGbuf[0]) ? dGbuf[1] : dGbuf[0];
-    for (int attempt = 0, pass = 0; attempt < 2; attempt++) {
+    for (int attempt = 0; attempt < 2; attempt++) {
       p = b + na + (haveP ? nP : 0);
       const int cw = p - b;  // |W| + |P|
       ColPtrs S, T;
@@ -1440,7 +1340,6 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
       ccols(WW, act, S, b);
       if (haveP) ccols(sP, actP, S, b + na);
       const bool full = force_full || (c->gram_refresh > 0 && (it % c->gram_refresh) == c->gram_refresh - 1);
-      bool used_derive = false;
       if (full) {  // periodic full Gram S^H [S AS]: no assumption on X (guards against drift)
         for (int t = 0; t < p; t++) T.p[t] = S.p[t];
         ccols(sAX, all, T, p);
@@ -1448,35 +1347,6 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         if (haveP) ccols(sAP, actP, T, p + b + na);
         Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * p * 2 * p, 16.0 * len * 2 * p);
         launch_gram(S, p, T, 2 * p, len, dG, c->gpart.as<cplx>(), st);
-      } else if (fused_ready) {
-        // the previous update pass left [X W P]^H [W P AP] and (AX)^H W for all nw columns: only
-        // W_a^H A W_a (A W exists since this iteration's apply) is new
-        ColPtrs Wa, AWa;
-        ccols(WW, act, Wa, 0);
-        ccols(AWW, act, AWa, 0);
-        Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * na * na, 16.0 * len * 2 * na);
-        launch_gram(Wa, na, AWa, na, len, dGww, c->gpart.as<cplx>(), st);
-        for (int t = 0; t < na; t++) hAct[t] = act[t];
-        cudaMemcpyAsync(dAct, hAct, na * sizeof(int), cudaMemcpyHostToDevice, st);
-        launch_ug_assemble(dUgRed, b, nw, dAct, na, haveP ? 1 : 0, dGww, dLam, p, dG, st);
-      } else if (c->gram_derive && haveP && g_prev && nP > 0 && pass == 0 &&
-                 b + na + nP <= 80 && p_prev <= 80) {
-        // S^H [W AW] from the vectors; X^H P, P^H P, X^H AP, P^H AP from the previous Gram and Ritz
-        // coefficients (P = S0 C0P, X = S0 C0); X^H X = I, X^H A X = Lambda as below
-        ColPtrs T;
-        ccols(WW, act, T, 0);
-        ccols(AWW, act, T, na);
-        {
-          Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * na, 16.0 * len * (p + na));
-          launch_gram(S, p, T, 2 * na, len, dGp, c->gpart.as<cplx>(), st);
-        }
-        for (int t = 0; t < nP; t++) hActP[t] = actP[t];
-        cudaMemcpyAsync(dActP, hActP, nP * sizeof(int), cudaMemcpyHostToDevice, st);
-        c->launches += 1;
-        if (launch_gram_derive(dG0, p_prev, dC, dActP, nP, dGp, na, dLam, b, dG, dCancel, st) != 0)
-          return set_err(PC_EINVAL, "gram_derive: sizes out of range");
-        cudaMemcpyAsync(hCancel, dCancel, sizeof(double), cudaMemcpyDeviceToHost, st);
-        used_derive = true;
       } else {
         // only the blocks that are not known: S^H [W P AW AP]; X^H X = I and X^H A X = Lambda hold for
         // the Ritz vectors X of the previous step, the rest follows by Hermitian symmetry
@@ -1484,50 +1354,11 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         ccols(AWW, act, T, cw);
         if (haveP) ccols(sAP, actP, T, cw + na);
         Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * p * 2 * cw, 16.0 * len * (p + cw));
-        int gt = -1;
-        if (c->gram_tmap && !c->gram_herm) {
-          // the five blocks as column ranges of their slots (holes = soft-locked columns)
-          GtBlocks gb;
-          memset(&gb, -1, sizeof(gb));
-          gb.ld = len;
-          const int slots[5] = {sX, WW, sP, AWW, sAP};
-          const std::vector<int>* lists[5] = {&all, &act, &actP, &act, &actP};
-          const int lofs[5] = {0, b, b + na, -1, -1}, tofs[5] = {-1, 0, na, cw, cw + na};
-          for (int kb = 0; kb < 5; kb++) {
-            const std::vector<int>& L = *lists[kb];
-            gb.base[kb] = col(slots[kb], 0);
-            gb.slot_cols[kb] = b;
-            gb.c0[kb] = 0;
-            gb.nc[kb] = 0;
-            if (L.empty() || ((kb == 2 || kb == 4) && !haveP)) continue;
-            gb.c0[kb] = L.front();
-            gb.nc[kb] = L.back() - L.front() + 1;
-            for (size_t t = 0; t < L.size(); t++) {
-              const int j = L[t] - L.front();
-              gb.lidx[kb][j] = (signed char)(lofs[kb] >= 0 ? lofs[kb] + (int)t : -1);
-              gb.tidx[kb][j] = (signed char)(tofs[kb] >= 0 ? tofs[kb] + (int)t : -1);
-            }
-          }
-          gt = launch_gram_tmap(gb, len, dGp, c->gpart.as<cplx>(), st);
-        }
-        if (gt < 0) launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st, c->gram_herm ? b : -1, cw);
+        launch_gram(S, p, T, 2 * cw, len, dGp, c->gpart.as<cplx>(), st);
         launch_gram_assemble(dGp, dLam, b, cw, dG, st);
       }
       rank = rr(p);
-      if (used_derive) {
-        last_cancel = *hCancel;
-        if (!(last_cancel <= c->derive_tau)) {
-          // the derived P blocks lost too many digits to cancellation: form this Gram from the vectors
-          // (the Rayleigh-Ritz above is discarded; dG0 and dC of the previous step are not needed again)
-          c->derive_fallbacks += 1;
-          pass = 1;
-          attempt--;
-          continue;
-        }
-      }
-      pass = 0;
-      p_prev = p;
-      g_prev = true;
+      if (rank < 0) return rank;
       if (rank >= p || (rank >= b && !c->p_restart)) break;
       if (rank >= b && !haveP) break;
       if (!haveP) return set_err(PC_ENUMERIC, "pc_bands: Rayleigh-Ritz basis collapsed (rank " +
@@ -1559,21 +1390,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
         if (!wr[j]) Y1.p[j] = Y1a.p[j] = nullptr;
         hasP[j] = wr[j];
       }
-      if (ug_ok) {
-        // both updates + the next residual + W + the next iteration's Gram blocks in one pass
-        const UgFlops uf = ug_flops(b, nw);
-        Prof pf(c, PC_STAT_UPDATE, st, 3, 2 * 8.0 * len * p * b + 84.0 * c->n3 * b + uf.flops_per_row * len,
-                16.0 * len * (2 * p + 2 * (b + nw) + nw));
-        MutColPtrs W;
-        mcols(WW, all, W, 0);
-        for (int j = nw; j < b; j++) W.p[j] = nullptr;
-        for (int j = 0; j < b; j++) hasW[j] = j < nw;
-        const int g = launch_update_gram(S, AS, p, dC, p, b, nw, Y2, Y1, Y2a, Y1a, W, dLam, c->n, c->d_ktab,
-                                         c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, dUgPart, dUgRed, rg, st);
-        launch_reduce_partial(dPart, g, b, dNorm, st);
-        resid_ready = true;
-        fused_ready = true;
-      } else if (c->fuse_resid) {
+      if (c->fuse_resid) {
         // both updates + the next residual R = AX' - X' Lambda', W = K_P^{-1} R (each row tile's W is
         // read into shared memory by the S phase before the same CTA overwrites it), |R|^2, |X'|^2
         Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * p * b + 84.0 * c->n3 * b,
@@ -1608,11 +1425,8 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
                                  c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         }
         if (g < 0)
-          g = c->update_stream
-                  ? launch_update_stream(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
-                                         c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st)
-                  : launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab,
-                                      c->cur_gamma, c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
+          g = launch_update_all(S, AS, p, dC, p, b, b, Y1, Y2, Y1a, Y2a, W, dLam, c->n, c->d_ktab, c->cur_gamma,
+                                c->cur_thr, deflate ? 1 : 0, dPart, rg, st);
         launch_reduce_partial(dPart, g, b, dNorm, st);
         resid_ready = true;
       } else {
@@ -1643,6 +1457,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
     normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, st>>>(X, dNorm, Y, len);
   }
   CU(cudaStreamSynchronize(st));
+  CU(cudaGetLastError());
   if (c->profile) prof_flush(c);
   for (int j = 0; j < nev; j++) {
     omega2[j] = hN[2 * b + j];

@@ -234,13 +234,9 @@ bool plane_supported(int n) { return n == PL_N; }
 cudaError_t launch_plane(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                          const EpsCoef& ec, const cplx* tw, cudaStream_t st) {
   if (n != PL_N || mode < 0 || mode > 2) return cudaErrorInvalidValue;
-  static bool attr[3] = {false, false, false};  // per MODE instance (the kernels share one type)
   auto run = [&](auto kern) -> cudaError_t {
-    if (!attr[mode]) {
-      cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)PL_SMEM);
-      if (e != cudaSuccess) return e;
-      attr[mode] = true;
-    }
+    cudaError_t e = smem_attr((const void*)kern, (int)PL_SMEM);
+    if (e != cudaSuccess) return e;
     kern<<<dim3(PL_CL * PL_N, ncols), PL_NT, PL_SMEM, st>>>(in, out, mask, ec, tw);
     return cudaGetLastError();
   };

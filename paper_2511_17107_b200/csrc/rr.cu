@@ -349,12 +349,7 @@ void launch_rr(const cplx* G, int p, int nb, double drop_tol, cplx* C, double* l
                cudaStream_t st) {
   const int np = (p + 1) & ~1;
   size_t smem = (size_t)2 * np * np * sizeof(cplx);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(rr_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
-    attr = true;
-  }
+  smem_attr((const void*)rr_kernel, (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
   rr_kernel<<<1, RR_THREADS, smem, st>>>(G, p, nb, drop_tol, C, lambda, info, scratch, g_jacobi_tol);
 }
 
@@ -390,11 +385,6 @@ __global__ void __launch_bounds__(RR_THREADS) heevj_kernel(const cplx* __restric
 void launch_heevj(const cplx* A, int n, double* w, cplx* V, int* info, cudaStream_t st) {
   const int np = (n + 1) & ~1;
   size_t smem = (size_t)2 * np * np * sizeof(cplx);
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(heevj_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
-    attr = true;
-  }
+  smem_attr((const void*)heevj_kernel, (int)(2 * RR_MAXN * RR_MAXN * sizeof(cplx)));
   heevj_kernel<<<1, RR_THREADS, smem, st>>>(A, n, w, V, info);
 }

@@ -13,7 +13,6 @@
 #include "kernels.h"
 #include "dmma.cuh"
 #include "kp.cuh"
-#include "tma.cuh"
 
 #ifndef PC_UA_SEG
 #define PC_UA_SEG 16
@@ -31,12 +30,7 @@ HD int ua_pitch4mod8(int p) {
   return x;
 }
 
-// TMA = true: the row tiles arrive by bulk copies (one 256-B run per column and component, issued by
-// warp 0, completion counted on one mbarrier per buffer) instead of per-thread 16-B cp.async.
-// CPT = true ("compact"): no shared copy of C (its fragments come through the L1 with __ldg) and an
-// unpadded tile pitch of 48 rows with an XOR row swizzle, 55 KB instead of 67 KB of shared memory per
-// CTA: 4 CTAs per SM instead of 3.
-template <int NT, bool TMA, bool CPT>
+template <int NT>
 __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) update_all_kernel(
     ColPtrs S, ColPtrs AS, int p, const cplx* __restrict__ C, int ldc, int r, int split, MutColPtrs Y1s,
     MutColPtrs Y2s, MutColPtrs Y1a, MutColPtrs Y2a, MutColPtrs Wout, const double* __restrict__ lam, int n,
@@ -44,57 +38,25 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
   constexpr int NTW = (NT + 1) / 2;
   extern __shared__ __align__(16) double uasm[];
   __shared__ double red[UA_WARPS][NTW][4][2][2];
-  __shared__ __align__(8) unsigned long long mbar[2];
   const int n3 = n * n * n;
   const int pe = (p + 3) & ~3;
   const int PS = ua_pitch4mod8(pe);
-  constexpr int RP = CPT ? UA_ROWS : UA_RP;
-  static_assert(!(TMA && CPT), "bulk copies need the unswizzled layout");
-  // tile element (column m, row rho): CPT swizzles rows within aligned groups of 8 so that the four
-  // columns of an A fragment (m & 3 = 0..3) land in distinct banks despite the 48-row pitch
-  auto RI = [](int m, int rho) { return m * RP + (CPT ? (rho ^ (2 * (m & 3))) : rho); };
+  constexpr int RP = UA_RP;
+  auto RI = [](int m, int rho) { return m * RP + rho; };
   cplx* Buf = reinterpret_cast<cplx*>(uasm);  // [2][pe][RP]: buffer 0 = S tiles, 1 = AS tiles
-  cplx* Cs = Buf + 2 * pe * RP;               // [NT*8][PS] (not with CPT)
+  cplx* Cs = Buf + 2 * pe * RP;               // [NT*8][PS]
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int rg = warp % UA_RG, ng = warp / UA_RG;
 
   for (int e = tid; e < NT * 8 * pe; e += UA_THREADS) {
     int c = e / pe, m = e % pe;
-    if (!CPT) Cs[c * PS + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
+    Cs[c * PS + m] = (c < r && m < p) ? C[(size_t)c * ldc + m] : mk(0, 0);
   }
   const long long ntiles = (n3 + UA_SEG - 1) / UA_SEG;
   const cplx* dummy = S.p[0];
-  unsigned phase[2] = {0u, 0u};
-  if constexpr (TMA) {
-    // padding columns [p, pe) are never written by the bulk copies: zero them once (0 * NaN = NaN)
-    for (int e = tid; e < 2 * (pe - p) * UA_RP; e += UA_THREADS) {
-      const int b = e / ((pe - p) * UA_RP), rem = e % ((pe - p) * UA_RP);
-      Buf[b * pe * UA_RP + p * UA_RP + rem] = mk(0, 0);
-    }
-    if (tid == 0) {
-      mbar_init(&mbar[0], 1);
-      mbar_init(&mbar[1], 1);
-    }
-    fence_proxy_async();
-    __syncthreads();
-  }
   auto load_tile = [&](int buf, const ColPtrs& src, long long t) {
     const long long m0 = t * UA_SEG;
     cplx* dst = Buf + buf * pe * RP;
-    if constexpr (TMA) {
-      if (warp == 0) {
-        const int nv = (int)min((long long)UA_SEG, (long long)n3 - m0);
-        const unsigned bytes = (unsigned)nv * 16u;
-        fence_proxy_async();
-        if (lane == 0) mbar_arrive_expect_tx(&mbar[buf], bytes * 3u * (unsigned)p);
-        __syncwarp();
-        for (int e = lane; e < 3 * p; e += 32) {
-          const int m = e / 3, seg = e % 3;
-          tma_load_1d(dst + m * UA_RP + seg * UA_SEG, src.p[m] + (long long)seg * n3 + m0, bytes, &mbar[buf]);
-        }
-      }
-      return;
-    }
     for (int e = tid; e < UA_ROWS * pe; e += UA_THREADS) {
       const int m = e / UA_ROWS, rho = e % UA_ROWS;
       const int seg = rho / UA_SEG, rr = rho % UA_SEG;
@@ -132,14 +94,8 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
       for (int i = 0; i < NTW; i++) {
         const int nt = ng + 2 * i;
         if (nt >= NT) break;
-        cplx cv;
-        if constexpr (CPT) {
-          const int cc = nt * 8 + (lane >> 2);
-          cv = (in && cc < r) ? ldg(C + (size_t)cc * ldc + mm) : mk(0, 0);
-        } else {
-          cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
-          if (!in) cv = mk(0, 0);
-        }
+        cplx cv = Cs[(nt * 8 + (lane >> 2)) * PS + mm];
+        if (!in) cv = mk(0, 0);
         const double cs = cv.x + cv.y;
 #ifdef PC_UA_NOMMA  // timing experiment: memory traffic only (results wrong)
         if (cs != 12345.0) continue;
@@ -186,13 +142,8 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
       }
     };
     // ---- S phase (buffer 0)
-    if constexpr (TMA) {
-      mbar_wait(&mbar[0], phase[0]);
-      phase[0] ^= 1u;
-    } else {
-      cp_async_wait<1>();  // the S tile of t has landed (the AS tile may still stream)
-      __syncthreads();
-    }
+    cp_async_wait<1>();  // the S tile of t has landed (the AS tile may still stream)
+    __syncthreads();
     zero();
     kloop(Buf, split, p);
     store(Y1s, false);
@@ -201,14 +152,9 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
     __syncthreads();  // buffer 0 is free
     if (more) load_tile(0, S, t + gridDim.x);
     // ---- AS phase (buffer 1)
-    if constexpr (TMA) {
-      mbar_wait(&mbar[1], phase[1]);
-      phase[1] ^= 1u;
-    } else {
-      if (more) cp_async_wait<1>();
-      else cp_async_wait<0>();
-      __syncthreads();
-    }
+    if (more) cp_async_wait<1>();
+    else cp_async_wait<0>();
+    __syncthreads();
     zero();
     const cplx* Ac = Buf + pe * RP;
     kloop(Ac, split, p);
@@ -252,7 +198,7 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
     __syncthreads();  // buffer 1 is free
     if (more) load_tile(1, AS, t + gridDim.x);
   }
-  if constexpr (!TMA) cp_async_wait<0>();
+  cp_async_wait<0>();
 
   // deterministic reduction: lanes sharing (lane & 3) hold the same column -> xor over lane >> 2 bits
 #pragma unroll
@@ -284,25 +230,15 @@ __global__ void __launch_bounds__(UA_THREADS, (NT <= 2) ? 512 / UA_THREADS : 1) 
   }
 }
 
-static int g_update_tma = 0;  // pc_set_option "update_tma": 1 = bulk copies (measured slower: 256-B runs)
-void set_update_tma(int v) { g_update_tma = v ? 1 : 0; }
-
-static int g_update_cpt = 0;  // pc_set_option "update_compact": 1 = CPT kernel (4 CTAs per SM; measured slower)
-void set_update_compact(int v) { g_update_cpt = v ? 1 : 0; }
-
-template <int NT, bool TMA, bool CPT>
+template <int NT>
 static int run_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C, int ldc, int r, int split,
                           const MutColPtrs& Y1s, const MutColPtrs& Y2s, const MutColPtrs& Y1a,
                           const MutColPtrs& Y2a, const MutColPtrs& W, const double* lam, int n, const cplx* kt,
                           double gamma, double thr, int deflate0, double* partial, int max_grid, cudaStream_t st) {
   const int pe = (p + 3) & ~3, ps = ua_pitch4mod8(pe);
-  const size_t smem = (size_t)(2 * pe * (CPT ? UA_ROWS : UA_RP) + (CPT ? 0 : NT * 8 * ps)) * sizeof(cplx);
-  auto kern = update_all_kernel<NT, TMA, CPT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  const size_t smem = (size_t)(2 * pe * UA_RP + NT * 8 * ps) * sizeof(cplx);
+  auto kern = update_all_kernel<NT>;
+  smem_attr((const void*)kern, 200 * 1024);
   int occ = 0;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, UA_THREADS, smem);
   occ = std::max(1, std::min(8, occ));
@@ -319,10 +255,7 @@ int launch_update_all(const ColPtrs& S, const ColPtrs& AS, int p, const cplx* C,
                       const MutColPtrs& W, const double* lam, int n, const cplx* kt, double gamma, double thr,
                       int deflate0, double* partial, int max_grid, cudaStream_t st) {
 #define PC_UA_ARGS S, AS, p, C, ldc, r, split, Y1s, Y2s, Y1a, Y2a, W, lam, n, kt, gamma, thr, deflate0, partial, max_grid, st
-#define PC_UA(NT_)                                                 \
-  return g_update_tma ? run_update_all<NT_, true, false>(PC_UA_ARGS) \
-         : g_update_cpt ? run_update_all<NT_, false, true>(PC_UA_ARGS) \
-                        : run_update_all<NT_, false, false>(PC_UA_ARGS)
+#define PC_UA(NT_) return run_update_all<NT_>(PC_UA_ARGS)
   if (r <= 8) PC_UA(1);
   if (r <= 16) PC_UA(2);
   if (r <= 24) PC_UA(3);

@@ -346,11 +346,7 @@ static int run_update_tmap(const UtMaps& mp, const cplx* C, int ldc, int r, cons
   const int PS = ((mp.pe + 3) & ~7) + 4;
   const size_t smem = 1024 + (size_t)UT_STAGES * mp.pe * UT_COLB + (size_t)NT * 8 * PS * sizeof(cplx);
   auto kern = update_tmap_kernel<NT>;
-  static bool attr = false;
-  if (!attr) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
-    attr = true;
-  }
+  smem_attr((const void*)kern, 200 * 1024);
   int occ = 0;
   constexpr int UT_THREADS = UtGeom<NT>::THREADS;
   cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, kern, UT_THREADS, smem);

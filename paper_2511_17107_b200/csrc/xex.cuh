@@ -226,155 +226,3 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
     gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + k] = v;
   }, orow, false);
 }
-
-// Ring variant of the fused x-pass (process-wide option "xex_ring"): a CTA walks the SH = N / XR_STRIPS
-// y-rows of one z-plane strip in chunks of TP output rows, keeping the inverse-transformed rows in a ring
-// of R = TP + 2 row slots per component (slot = q mod R, q = row index within the strip's halo'd range).
-// Each input row is read from HBM and inverse-transformed once: the halo rows of a chunk (E^1 at y0-1,
-// E^2 at y0+TP, MODE 1 only) come from the previous chunk -- E^2's from the ring, E^1's (an output row of
-// the previous chunk, overwritten by its forward DFT) from a spare row saved before the write-back.
-// Only the first chunk of a strip loads the two halo rows (2 per SH rows instead of 2 per TP rows).
-#ifndef PC_XR_STRIPS
-#define PC_XR_STRIPS 2
-#endif
-template <int N>
-struct XrCfg {
-  static constexpr int TP = XexCfg<N>::TP;
-  static constexpr int R = TP + 2;
-  static constexpr int STRIPS = (N / TP) % PC_XR_STRIPS == 0 ? PC_XR_STRIPS : 1;
-  static constexpr int SH = N / STRIPS;               // rows per CTA
-  static constexpr int P = XRow<N>::P;
-  static constexpr int NT = XexCfg<N>::NT;
-  static constexpr int PPT = XexCfg<N>::PPT;
-  static constexpr size_t SMEM = (size_t)(3 * R + 2) * P * sizeof(cplx) + (size_t)N * sizeof(cplx) + (size_t)R * N;
-};
-
-template <int N, int MODE>
-__global__ void __launch_bounds__(XrCfg<N>::NT, PC_XEX_MINB)
-xexr_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
-            double scale, int zoff) {
-  using Cfg = XrCfg<N>;
-  constexpr int TP = Cfg::TP, R = Cfg::R, P = Cfg::P, NT = Cfg::NT, PPT = Cfg::PPT, SH = Cfg::SH;
-  constexpr int N3 = N * N * N;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* s = reinterpret_cast<cplx*>(smem_raw);  // ring row (c, slot) at s + (c * R + slot) * P
-  cplx* spare = s + 3 * R * P;                  // 2 rows: E^1 halo of the next chunk (double-buffered)
-  cplx* tw = spare + 2 * P;
-  uint8_t* mk8 = reinterpret_cast<uint8_t*>(tw + N);  // mask rows by slot
-  const int tid = threadIdx.x;
-  const int z = zoff + blockIdx.x / Cfg::STRIPS, ys = (blockIdx.x % Cfg::STRIPS) * SH;
-  const cplx* gin = in.p[blockIdx.y];
-  cplx* gout = out.p[blockIdx.y];
-  auto gy = [&](int q) { return (ys - 1 + q + N) % N; };  // q = 0 .. SH + 1 <-> y = ys - 1 .. ys + SH
-  auto slot = [](int q) { return q % R; };
-  xrow_twiddles<N>(tw, twg);
-
-  for (int ci = 0; ci < SH / TP; ci++) {
-    const int q0 = 1 + ci * TP;  // first output row
-    __syncthreads();             // previous chunk's forward DFT is done with the ring
-    // mask rows q0-1 .. q0+TP
-    for (int e = tid; e < (TP + 2) * N; e += NT) {
-      const int q = q0 - 1 + e / N, x = e % N;
-      mk8[slot(q) * N + x] = __ldg(mask + ((long long)z * N + gy(q)) * N + x);
-    }
-    // pencils to inverse-transform: (component, q) lists
-    //   MODE 1, first chunk: E1 q0-1 .. q0+TP-1, E2 q0 .. q0+TP, E3 q0 .. q0+TP-1
-    //   MODE 1, later:       E1 q0 .. q0+TP-1,   E2 q0+1 .. q0+TP, E3 q0 .. q0+TP-1
-    //   MODE 0/2:            all three q0 .. q0+TP-1
-    const bool first = (ci == 0);
-    const int n1 = (MODE == 1 && first) ? TP + 1 : TP;
-    const int n2 = (MODE == 1 && first) ? TP + 1 : TP;
-    const int a1 = (MODE == 1 && first) ? q0 - 1 : q0;  // first q of E1
-    const int a2 = (MODE == 1) ? (first ? q0 : q0 + 1) : q0;
-    auto pq = [&](int pen, int& c, int& q) {
-      if (pen < n1) { c = 0; q = a1 + pen; }
-      else if (pen < n1 + n2) { c = 1; q = a2 + pen - n1; }
-      else { c = 2; q = q0 + pen - n1 - n2; }
-    };
-    auto prow = [&](int pen) { int c, q; pq(pen, c, q); return c * R + slot(q); };
-    auto gload = [&](int pen, int j) {
-      int c, q;
-      pq(pen, c, q);
-      return ldg(gin + (long long)c * N3 + ((long long)z * N + gy(q)) * N + j);
-    };
-    const int npen = n1 + n2 + TP;
-    xrow_step1<N, +1, decltype(gload), decltype(prow), true>(s, tw, npen, gload, prow, false);
-    __syncthreads();
-    xrow_step2<N, +1>(s, npen, [&](int pen, int k, cplx v) { s[prow(pen) * P + k] = v; }, prow, true);
-    __syncthreads();
-
-    // M_eps on the TP output rows (registers first); E1 row q0+TP-1 saved for the next chunk's halo
-    cplx* e1prev = spare + ((ci + 1) & 1) * P;  // E1 row q0-1 (written by the previous chunk)
-    if constexpr (MODE == 1) {
-      cplx* e1save = spare + (ci & 1) * P;
-      for (int x = tid; x < N; x += NT) e1save[x] = s[(0 * R + slot(q0 + TP - 1)) * P + x];
-    }
-    cplx w[PPT][3];
-#pragma unroll
-    for (int t = 0; t < PPT; t++) {
-      const int e = tid + t * NT;
-      if (e >= N * TP) break;
-      const int x = e % N, q = q0 + e / N;
-      const uint8_t mp = mk8[slot(q) * N + x];
-      const double i1 = (mp & 1) ? 1.0 : 0.0, i2 = (mp & 2) ? 1.0 : 0.0, i3 = (mp & 4) ? 1.0 : 0.0;
-      const cplx v1 = s[(0 * R + slot(q)) * P + x], v2 = s[(1 * R + slot(q)) * P + x], v3 = s[(2 * R + slot(q)) * P + x];
-      cplx w1 = (1.0 + ec.d[0] * i1) * v1, w2 = (1.0 + ec.d[1] * i2) * v2, w3 = (1.0 + ec.d[2] * i3) * v3;
-      if (MODE == 1) {
-        const int xm = (x == 0) ? N - 1 : x - 1, xp = (x == N - 1) ? 0 : x + 1;
-        // S_12 v2 (into w1): points {x-1, x} x {y, y+1}, weight I1(p) + I2(q)
-        cplx acc = mk(0, 0);
-        const int qx[2] = {xm, x};
-#pragma unroll
-        for (int aa = 0; aa < 2; aa++)
-#pragma unroll
-          for (int bb = 0; bb < 2; bb++) {
-            const int qq = q + bb, xx = qx[aa];
-            const double wgt = i1 + ((mk8[slot(qq) * N + xx] & 2) ? 1.0 : 0.0);
-            acc = acc + wgt * s[(1 * R + slot(qq)) * P + xx];
-          }
-        w1 = w1 + 0.125 * cmul(ec.e[0], acc);
-        // S_12^T v1 (into w2): points {x, x+1} x {y-1, y}, weight I1(q) + I2(p)
-        cplx acc2 = mk(0, 0);
-        const int qx2[2] = {x, xp};
-#pragma unroll
-        for (int aa = 0; aa < 2; aa++)
-#pragma unroll
-          for (int bb = 0; bb < 2; bb++) {
-            const int qq = q - 1 + bb, xx = qx2[aa];
-            const double wgt = i2 + ((mk8[slot(qq) * N + xx] & 1) ? 1.0 : 0.0);
-            const cplx ev = (qq == q0 - 1 && !first) ? e1prev[xx] : s[(0 * R + slot(qq)) * P + xx];
-            acc2 = acc2 + wgt * ev;
-          }
-        w2 = w2 + 0.125 * cmul(conjg(ec.e[0]), acc2);
-      } else if (MODE == 2) {
-        if (mp & 8) {
-          w1 = w1 + cmul(ec.e[0], v2) + cmul(ec.e[1], v3);
-          w2 = w2 + cmul(conjg(ec.e[0]), v1) + cmul(ec.e[2], v3);
-          w3 = w3 + cmul(conjg(ec.e[1]), v1) + cmul(conjg(ec.e[2]), v2);
-        }
-      }
-      w[t][0] = scale * w1;
-      w[t][1] = scale * w2;
-      w[t][2] = scale * w3;
-    }
-    __syncthreads();
-#pragma unroll
-    for (int t = 0; t < PPT; t++) {
-      const int e = tid + t * NT;
-      if (e >= N * TP) break;
-      const int x = e % N, q = q0 + e / N;
-#pragma unroll
-      for (int c = 0; c < 3; c++) s[(c * R + slot(q)) * P + x] = w[t][c];
-    }
-    __syncthreads();
-
-    // forward x-DFT of the TP output rows; the last step writes HBM directly
-    auto orow = [&](int pen) { return (pen / TP) * R + slot(q0 + pen % TP); };
-    auto sload = [&](int pen, int j) { return s[orow(pen) * P + j]; };
-    xrow_step1<N, -1, decltype(sload), decltype(orow), true>(s, tw, 3 * TP, sload, orow, true);
-    xrow_step2<N, -1>(s, 3 * TP, [&](int pen, int k, cplx v) {
-      const int c = pen / TP, r = pen % TP;
-      gout[(long long)c * N3 + ((long long)z * N + gy(q0 + r)) * N + k] = v;
-    }, orow, false);
-  }
-}

@@ -139,28 +139,6 @@ def test_apply_fourier_matches_oracle(api, lat, geo, eps, mode, n, k):
     assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-12
 
 
-@pytest.mark.parametrize("lat,geo,eps,mode,n,k", APPLY_CASES + [("fcc", "fcc_diamond", "pc", "crossdof", 128, (PI, PI, PI)),
-                                                   ("sc", "sc_curv", "pc", "trivial", 64, (0.3, 0.2, 0.1))])
-def test_apply_xex_ring_matches_oracle(api, lat, geo, eps, mode, n, k):
-    """Process-wide option xex_ring = 1 (ring variant of the fused x-pass: each row inverse-transformed
-    once, halo rows carried between chunks) against the oracle, every mode, n up to 128."""
-    A = synth.lattice(lat)
-    e = _eps(eps)
-    masks = synth.make_masks(geo, A, n, seed=11)
-    ctx = api.pc_create(A, n, e, masks, eps_mode=mode)
-    nc = 1 if n >= 64 else 2
-    x = synth.random_block(n, nc, seed=5)
-    Y = torch.empty(nc, 3 * n ** 3, dtype=torch.complex128, device="cuda")
-    api.pc_set_option(ctx, "xex_ring", 1)
-    try:
-        api.pc_apply(ctx, k, to_dev(x), Y)
-        torch.cuda.synchronize()
-    finally:
-        api.pc_set_option(ctx, "xex_ring", 0)
-    op = O.PenalizedOperator(n, np.array(k), A, e, masks, mode)
-    assert relerr_cols(Y.cpu().numpy(), op.apply_fourier(x)) <= 1e-12
-
-
 @pytest.mark.parametrize("lat,n,k", [("sc", 8, (0.4, 0.1, -0.3)), ("fcc", 12, (PI, PI, PI))])
 def test_apply_real_space_matches_oracle(api, lat, n, k):
     A = synth.lattice(lat)

@@ -1,7 +1,7 @@
-"""k-point throughput of concurrent solves (bands.solve_concurrent) vs the persistent-grid share
-(option grid_frac) and the number of contexts per GPU, on the bench workload.
+"""k-point throughput of concurrent solves (bands.solve_concurrent) vs the number of contexts per GPU,
+on the bench workload.
 
-usage: python tools/conc_sweep.py [--nk 6] [--fracs 1 0.5] [--streams 2 3] [--key value ...]
+usage: python tools/conc_sweep.py [--nk 6] [--streams 2 3] [--opt key value ...]
 """
 import argparse
 import json
@@ -18,7 +18,6 @@ from paper_2511_17107_b200 import api, bands  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--workload", default="C4")
 ap.add_argument("--nk", type=int, default=6)
-ap.add_argument("--fracs", type=float, nargs="+", default=[1.0, 0.67, 0.5])
 ap.add_argument("--streams", type=int, nargs="+", default=[2, 3])
 ap.add_argument("--opt", nargs=2, action="append", default=[], help="extra pc_set_option key value")
 a = ap.parse_args()
@@ -33,12 +32,9 @@ for c in ctxs:
         api.pc_set_option(c, k, float(v))
 bands.solve_concurrent(ctxs[:2], kp, [0, 0], W.nev, 1e-5, 15, 0)  # warm-up (workspaces, JIT)
 for s in a.streams:
-    for f in a.fracs:
-        api.pc_set_option(ctxs[0], "grid_frac", f)
-        torch.cuda.synchronize()
-        t = time.time()
-        om, rs, it, st = bands.solve_concurrent(ctxs[:s], kp, idx, W.nev, 1e-5, 1000, 0)
-        torch.cuda.synchronize()
-        el = time.time() - t
-        print(json.dumps({"streams": s, "grid_frac": f, "kpts_per_s": len(idx) / el, "iters": it.tolist()}),
-              flush=True)
+    torch.cuda.synchronize()
+    t = time.time()
+    om, rs, it, st = bands.solve_concurrent(ctxs[:s], kp, idx, W.nev, 1e-5, 1000, 0)
+    torch.cuda.synchronize()
+    el = time.time() - t
+    print(json.dumps({"streams": s, "kpts_per_s": len(idx) / el, "iters": it.tolist()}), flush=True)
