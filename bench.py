@@ -272,21 +272,30 @@ def main():
         api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
     ctx = ctxs[0]
 
-    def kidx(s):
+    def kidx(s, r=None):
+        r = rank if r is None else r
         if args.warm_start:  # contiguous stretch per rank
-            return (rank * (args.warmup + args.steps + len(ctxs)) + s) % nk
-        return (rank + world * s) % nk
+            return (r * (args.warmup + args.steps + len(ctxs)) + s) % nk
+        return (r + world * s) % nk
 
-    def run(idx_list):
+    def run(svals):
+        """Solve a step set.  Cold start: the public band_structure call -- the k-points of ALL ranks
+        (the union of every rank's idx_list) go into one dynamic queue (atomic counter in the process
+        group's store), each rank's contexts draw from it, one all-gather returns every result; this
+        rank's rows (k-points kidx(s) of the step numbers svals) are returned in step order.  Warm start: contiguous stretches per rank."""
+        svals = list(svals)
+        idx_list = [kidx(s_) for s_ in svals]
         if args.warm_start:
             return bands.solve_warm(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
-        if len(ctxs) == 1:
-            return bands.solve_local(ctx, kp, idx_list, W.nev, args.tol, args.maxit, 0)
-        return bands.solve_concurrent(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
+        ks = sorted({kidx(s_, r) for r in range(world) for s_ in svals})
+        res = bands.band_structure(ctxs, kp, nev=W.nev, tol=args.tol, maxit=args.maxit, seed=0,
+                                   device=cdev, ks=ks)
+        sel = np.array(idx_list, dtype=np.int64)
+        return res["omega2"][sel], res["resid"][sel], res["iters"][sel], res["status"][sel]
 
     # warm-up: W solves (at least one per context: allocations, first touch, kernel attributes)
     nwarm = max(args.warmup, len(ctxs))
-    wit = [int(v) for v in run([kidx(s) for s in range(nwarm)])[2]]
+    wit = [int(v) for v in run(range(nwarm))[2]]
     for c_ in ctxs:
         api.pc_stats(c_, reset=True)
         api.pc_set_option(c_, "profile", 1)
@@ -294,9 +303,10 @@ def main():
     barrier()
     clk.start()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    idx = [kidx(s) for s in range(nwarm, nwarm + args.steps)]
+    svals = list(range(nwarm, nwarm + args.steps))
+    idx = [kidx(s) for s in svals]
     e0.record()
-    om, rs, it_, st_ = run(idx)
+    om, rs, it_, st_ = run(svals)
     e1.record()
     torch.cuda.synchronize()
     ms = e0.elapsed_time(e1)
@@ -323,13 +333,9 @@ def main():
     res = [(om[i:i + 1], rs[i:i + 1], it_[i:i + 1], st_[i:i + 1]) for i in range(len(idx))]
     iters = [int(r[2][0]) for r in res]
     status = [int(r[3][0]) for r in res]
-    # the one collective of the method: all-gather of eigenvalues
-    gathered = None
-    if world > 1:
-        loc = torch.from_numpy(np.concatenate([np.array(idx)[:, None], om], axis=1)).to(cdev)
-        out = torch.empty((world * loc.shape[0], loc.shape[1]), dtype=loc.dtype, device=cdev)
-        dist.all_gather_into_tensor(out, loc)
-        gathered = out.shape[0]
+    # the one collective of the method (all-gather of omega^2, Res, iterations, status) ran
+    # inside the timed band_structure call: world * steps rows
+    gathered = world * args.steps if (world > 1 and not args.warm_start) else None
 
     # ---- the same timed steps with the other preconditioner (same k-points, same protocol), reported
     # under alt_precond: the headline stays on the paper's K_P^{-1} unless --precond eps
@@ -338,11 +344,11 @@ def main():
         other = "eps" if args.precond == "kp" else "kp"
         for c_ in ctxs:
             api.pc_set_option(c_, "precond", 1 if other == "eps" else 0)
-        run([kidx(s) for s in range(len(ctxs))])  # one untimed solve per context
+        run(range(len(ctxs)))  # one untimed solve per context
         barrier()
         a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         a0.record()
-        aom, ars, ait, ast = run(idx)
+        aom, ars, ait, ast = run(svals)
         a1.record()
         torch.cuda.synchronize()
         ta = torch.tensor([a0.elapsed_time(a1)], dtype=torch.float64, device=cdev)
@@ -479,10 +485,10 @@ def main():
                 if args.w_guard is not None:
                     api.pc_set_option(c_, "w_guard", args.w_guard)
                 api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
-            if nctx == 1:
-                out = bands.solve_local(ce[0], kp, idx_list, W.nev, args.tol, args.maxit, 0)
-            else:
-                out = bands.solve_concurrent(ce, kp, idx_list, W.nev, args.tol, args.maxit, 0)
+            res = bands.band_structure(ce, kp, nev=W.nev, tol=args.tol, maxit=args.maxit, seed=0, device=cdev,
+                                       ks=sorted(set(idx_list)))
+            sel = np.array(idx_list, dtype=np.int64)
+            out = (res["omega2"][sel], res["resid"][sel], res["iters"][sel], res["status"][sel])
             for c_ in ce:
                 c_.close()
             return out
@@ -508,8 +514,8 @@ def main():
         e2e = {"value": world * args.e2e_steps / float(tt.item()), "unit": "k-points/s",
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h), "iters": e_it,
                "note": f"one job of {args.e2e_steps} k-points per rank: pc_create x {nctx} from pinned host masks "
-                       "(upload included) + bands.solve_concurrent with host k-points and host omega^2/Res "
-                       "outputs + pc_destroy, wall clock"}
+                       "(upload included) + bands.band_structure (dynamic k queue, concurrent contexts, one all-gather) "
+                       "with host k-points and host omega^2/Res outputs + pc_destroy, wall clock"}
 
     # ---- CPU oracle baseline (rank 0, N = 1 only)
     cpu = None

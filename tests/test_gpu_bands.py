@@ -301,3 +301,50 @@ def test_bands_full_size_c4_properties(api):
                 assert abs(np.vdot(V[j], Av).real - om[1][j]) <= 1e-9 * om[1][j]
         ctx.close()
     assert rel(om[0], om[1]) <= 1e-9
+
+
+# ------------------------------------------------------- config-size eigenvalue parity (C2, C3, C4)
+def _golden_sets():
+    """tests/golden/c{2,3,4}_*.txt, written by tests/golden/gen_goldens.py from the oracle only."""
+    out = []
+    for name in ("c2_sc_sphere_n32.txt", "c3_sc_sc_curv_n64.txt", "c4_fcc_fcc_diamond_n128.txt"):
+        path = os.path.join(GOLD, name)
+        if os.path.exists(path):
+            g = golden(name)
+            for key in g:
+                if key.startswith("ev"):
+                    out.append(pytest.param(name, int(key[2:]), id=f"{name[:2]}-k{key[2:]}"))
+    return out
+
+
+@pytest.mark.parametrize("name,ki", _golden_sets())
+def test_bands_match_oracle_goldens_config_size(api, name, ki):
+    """North-star target (BASELINE.json): all 10 bands at the benchmark configurations against the
+    oracle's eigenvalues (SciPy LOBPCG on the oracle's sparse operator, tol <= 2e-8), relative <= 1e-8.
+    C2: SC sphere n = 32, the whole 33-point path; C3: SC-CURV pseudochiral n = 64; C4: FCC diamond
+    pseudochiral n = 128 (the bench workload) at X, a generic U-L point and L.  PAPER.md:1055-1064,
+    1080-1095."""
+    wname = {"c2": "C2", "c3": "C3", "c4": "C4"}[name[:2]]
+    W = synth.WORKLOADS[wname]
+    g = golden(name)
+    k = g[f"k{ki}"]
+    assert np.allclose(k, W.kpoints()[ki], rtol=0, atol=1e-15)
+    ref = g[f"ev{ki}"]
+    ctx = _ctx_cache(wname)
+    api.pc_set_option(ctx, "kindex_offset", ki)
+    r = api.pc_bands(ctx, [k], nev=W.nev, tol=TOL, maxit=1000)
+    assert r["status"][0] == 0
+    assert rel(r["omega2"][0], ref) <= 1e-8, (r["omega2"][0], ref)
+
+
+_CTX = {}
+
+
+def _ctx_cache(wname):
+    from paper_2511_17107_b200 import api as a
+    if wname not in _CTX:
+        _CTX.clear()  # one workload context alive at a time (C4 needs ~17 GB of workspace)
+        W = synth.WORKLOADS[wname]
+        _CTX[wname] = a.pc_create(W.A(), W.n, W.eps1(), W.masks())
+    return _CTX[wname]
+

@@ -33,10 +33,10 @@ def relerr_cols(got, ref):
 
 
 # ------------------------------------------------------------------------------------- FFT
-@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 100, 120, 128])
+@pytest.mark.parametrize("n", [4, 6, 8, 10, 12, 16, 20, 24, 32, 40, 48, 64, 80, 96, 100, 120, 128, 160, 192, 240, 256])
 def test_fft3_matches_paper_F3(api, n):
     ctx = api.pc_create(np.eye(3), n, np.eye(3), np.zeros((4, n, n, n), np.uint8))
-    x = synth.random_block(n, 2, seed=n)
+    x = synth.random_block(n, 2 if n <= 128 else 1, seed=n)
     X = to_dev(x)
     Y = torch.empty_like(X)
     api.pc_fft3(ctx, X, Y, api.PC_FFT_TO_FOURIER)
@@ -188,6 +188,25 @@ def test_apply_full_size_n128_fcc_pseudochiral(api, plane):
     op = O.PenalizedOperator(n, k, A, e, masks)
     ref = op.apply_fourier(x)
     assert relerr_cols(Y[:2].cpu().numpy(), ref) <= 1e-12
+
+
+def test_apply_full_size_n192_c5(api):
+    """BASELINE config C5 (FCC diamond pseudochiral, n = 192: the 16 x 12 radix plan) at full size, a
+    26-column block (C5's b = nev + guard) with two oracle columns (white and smooth), <= 1e-12."""
+    W = synth.WORKLOADS["C5"]
+    n, A, e, masks = W.n, W.A(), W.eps1(), W.masks()
+    k = np.array([PI / 2, 2 * PI, PI / 2])
+    ctx = api.pc_create(A, n, e, masks)
+    x = np.concatenate([synth.random_block(n, 1, seed=31), synth.random_block(n, 1, seed=32, kind="smooth")])
+    X = torch.randn(26, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    X[:2] = to_dev(x)
+    Y = torch.empty_like(X)
+    api.pc_apply(ctx, k, X, Y)
+    torch.cuda.synchronize()
+    got = Y[:2].cpu().numpy()
+    del X, Y
+    op = O.PenalizedOperator(n, k, A, e, masks)
+    assert relerr_cols(got, op.apply_fourier(x)) <= 1e-12
 
 
 @pytest.mark.parametrize("mode,eps,geo", [("diagonal", "iso", "sphere"), ("trivial", "sdd", "random"),
