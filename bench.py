@@ -107,18 +107,19 @@ class Clocks:
 
 
 # ------------------------------------------------------------------------------------------
-# CPU oracle timing (cpu_baseline and --impl reference)
+# CPU oracle timing (cpu_baseline and --impl reference): the oracle as it stands, in worker processes
+# (one per host core used, OMP_NUM_THREADS=1 each), on bounded samples of the workload.
 # ------------------------------------------------------------------------------------------
-def oracle_sample(W, k, nsample_cols=1, build=None, masks=None):
-    """Time the oracle as it stands on a bounded sample of one k-point solve of workload W:
-    sparse assembly (once per k), nsample_cols operator applies + K_P^{-1} solves, and one
-    Rayleigh-Ritz Gram of the 3b-column block.  Returns the component times."""
+def oracle_sample(W, k, nsample_cols=1, masks=None):
+    """Time the oracle on a bounded sample of one k-point solve of workload W: sparse assembly of
+    Op(k), nsample_cols Fourier-space applies + K_P^{-1} solves, and one Rayleigh-Ritz Gram of the
+    3b-column block (b = nev + 5, the oracle's guard).  Returns the component times."""
     from oracle import pc_oracle as O
     import synth
     t0 = time.perf_counter()
     if masks is None:
         masks = W.masks()
-    op = build if build is not None else O.PenalizedOperator(W.n, k, W.A(), W.eps1(), masks)
+    op = O.PenalizedOperator(W.n, k, W.A(), W.eps1(), masks)
     t_asm = time.perf_counter() - t0
     x = synth.random_block(W.n, nsample_cols, seed=3)
     t0 = time.perf_counter()
@@ -134,49 +135,144 @@ def oracle_sample(W, k, nsample_cols=1, build=None, masks=None):
     t0 = time.perf_counter()
     S.conj().T @ np.concatenate([S, S], axis=1)
     t_gram = (time.perf_counter() - t0) * (op.dim / rows)
-    return op, {"assembly_s": t_asm, "apply_s_per_col": t_apply, "precond_s_per_col": t_prec,
-                "gram_s": t_gram, "block": b}
+    return {"assembly_s": t_asm, "apply_s_per_col": t_apply, "precond_s_per_col": t_prec,
+            "gram_s": t_gram, "block": b}
 
 
-def oracle_kpts_per_s(t, iters):
+def oracle_kpoint_s(t, iters):
     """Model of one oracle k-point solve: assembly + iters x (b applies + b K_P^{-1} + 2 Grams)."""
     b = t["block"]
     per_it = b * (t["apply_s_per_col"] + t["precond_s_per_col"]) + 2.0 * t["gram_s"]
-    return 1.0 / (t["assembly_s"] + iters * per_it), per_it
+    return t["assembly_s"] + iters * per_it, per_it
+
+
+def oracle_iters(W):
+    """The ORACLE's own LOBPCG iteration count on this workload (tests/diag/oracle_iters.py, committed
+    under profiles/): SciPy LOBPCG on the oracle operator, tol 1e-5, guard 5.  None if not measured."""
+    d = load_json(os.path.join(ROOT, "profiles", f"oracle_iters_{W.name.lower()}.json"), None)
+    if not d or not d.get("rows"):
+        return None, None
+    its = [r["iterations"] for r in d["rows"]]
+    return float(np.mean(its)), f"profiles/oracle_iters_{W.name.lower()}.json ({d['rows'][0]['tol']:g}, k {[r['kidx'] for r in d['rows']]})"
+
+
+def oracle_worker(args):
+    """--oracle-worker (a subprocess, OMP_NUM_THREADS=1): component sample of workload args.workload at
+    path point args.kidx, and optionally one complete oracle solve of a C2 path point (args.c2k)."""
+    import synth
+    from oracle import pc_oracle as O
+    W = synth.WORKLOADS[args.workload]
+    out = {"kidx": args.kidx, "components": oracle_sample(W, W.kpoints()[args.kidx])}
+    if args.c2k >= 0:
+        W2 = synth.WORKLOADS["C2"]
+        t0 = time.perf_counter()
+        op = O.PenalizedOperator(W2.n, W2.kpoints()[args.c2k], W2.A(), W2.eps1(), W2.masks())
+        info = {}
+        ev, res = O.eigs_iterative(op, W2.nev, tol=args.tol, seed=1000 + args.c2k, maxiter=600, guard=5, info=info)
+        out["c2"] = {"kidx": args.c2k, "seconds": time.perf_counter() - t0, "iterations": info.get("iterations"),
+                     "max_res": float(res.max())}
+    print(json.dumps(out), flush=True)
+
+
+def oracle_parallel(args, kidx_list, c2_list=None):
+    """Run len(kidx_list) oracle workers at once (one per core, OMP_NUM_THREADS=1 each); returns their
+    JSON results and the wall time."""
+    env = dict(os.environ, OMP_NUM_THREADS="1", OPENBLAS_NUM_THREADS="1", MKL_NUM_THREADS="1")
+    for k in ("RANK", "LOCAL_RANK", "WORLD_SIZE"):
+        env.pop(k, None)
+    procs = []
+    t0 = time.perf_counter()
+    for i, ki in enumerate(kidx_list):
+        cmd = [sys.executable, os.path.join(ROOT, "bench.py"), "--oracle-worker", "--workload", args.workload,
+               "--kidx", str(ki), "--tol", str(args.tol), "--c2k", str(c2_list[i] if c2_list else -1)]
+        procs.append(subprocess.Popen(cmd, env=env, stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True))
+    outs = []
+    for pr in procs:
+        o, _ = pr.communicate()
+        lines = [ln for ln in o.splitlines() if ln.startswith("{")]
+        if pr.returncode != 0 or not lines:
+            raise RuntimeError(f"oracle worker failed (rc {pr.returncode})")
+        outs.append(json.loads(lines[-1]))
+    return outs, time.perf_counter() - t0
+
+
+def host_cores():
+    return len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else (os.cpu_count() or 1)
+
+
+def cpu_model():
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_baseline(args, W, steps_kidx, with_c2):
+    """Oracle k-points/s on the host cores: nw = min(cores, 8) worker processes each time a component
+    sample of a different k-point; a k-point's time is extrapolated with the oracle's own iteration
+    count; value = nw / mean k-point time (nw k-points solved side by side).  with_c2: each worker also
+    solves one C2 path point completely (a real oracle solve, no model): C2 k-points/s = nw / wall."""
+    nw = max(1, min(host_cores(), 8))
+    its, its_src = oracle_iters(W)
+    nk = len(W.kpoints())
+    kl = [steps_kidx[i % len(steps_kidx)] for i in range(nw)]
+    c2l = [(3 * i + 1) % 33 for i in range(nw)] if with_c2 else None
+    outs, wall = oracle_parallel(args, kl, c2l)
+    comps = [o["components"] for o in outs]
+    if its is None:
+        its, its_src = PAPER_ITERS_FCC_PC, "PAPER.md:1199 (oracle count not measured)"
+    ks = [oracle_kpoint_s(c, its)[0] for c in comps]
+    value = nw / float(np.mean(ks))
+    res = {"value": value, "unit": "k-points/s", "cores": nw, "kind": "oracle", "cpu": cpu_model(),
+           "sample": (f"{nw} oracle worker processes (OMP_NUM_THREADS=1), each: sparse assembly of Op(k) at "
+                      f"n={W.n} + 1 Fourier-space apply + 1 K_P^-1 column + one 3b-column Gram (b = nev + 5) "
+                      f"at its own {W.name} path point; k-point time = assembly + {its:.0f} iterations (the oracle's "
+                      f"own SciPy LOBPCG count, {its_src}) x (b applies + b K_P^-1 + 2 Grams); "
+                      f"value = {nw} / mean k-point time"),
+           "components_mean": {k: float(np.mean([c[k] for c in comps])) for k in comps[0]},
+           "kpoint_s_mean": float(np.mean(ks)), "wall_s": wall, "nk_path": nk}
+    if with_c2:
+        c2 = [o["c2"] for o in outs]
+        res["c2_measured"] = {"value": nw / max(c["seconds"] for c in c2), "unit": "k-points/s",
+                              "what": f"{nw} complete oracle solves of C2 path points (SC sphere, n = 32, 10 bands, "
+                                      f"tol {args.tol:g}) side by side, k-points / wall (no model)",
+                              "iterations": [c["iterations"] for c in c2],
+                              "seconds": [round(c["seconds"], 2) for c in c2]}
+    res["paper_timings"] = ("context only: PAPER.md:1260 pseudochiral FCC N=120, 10 bands at (pi,pi,pi): "
+                            "GPU 34.15 s (RTX 4090 D, cupy; 0.029 k-points/s), CPU 1506.35 s (numpy, CPU "
+                            "model not stated; 0.00066 k-points/s), 55 LOBPCG steps")
+    return res
 
 
 def run_reference(args):
-    """--impl reference: the CPU oracle arm (rank 0 only; other ranks exit 0)."""
+    """--impl reference: the CPU oracle arm (rank 0 only; other ranks exit 0).  Each step = one round of
+    oracle workers (one per host core used) timing a component sample of different C4 path points."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
     import synth
     W = synth.WORKLOADS[args.workload]
-    kp = W.kpoints()
-    cores = len(os.sched_getaffinity(0)) if hasattr(os, "sched_getaffinity") else os.cpu_count()
-    masks = W.masks()
-    times = []
-    comps = []
+    nk = len(W.kpoints())
+    times, vals, last = [], [], None
     for s in range(args.warmup + args.steps):
-        k = kp[s % len(kp)]
         t0 = time.perf_counter()
-        op, t = oracle_sample(W, k, 1, masks=masks)
+        r = oracle_baseline(args, W, [(s * 8 + i) % nk for i in range(8)], with_c2=False)
         el = time.perf_counter() - t0
         if s >= args.warmup:
             times.append(el)
-            comps.append(t)
-    vals = [oracle_kpts_per_s(t, PAPER_ITERS_FCC_PC)[0] for t in comps]
+            vals.append(r["value"])
+            last = r
     value = float(np.mean(vals))
-    sample = (f"per step: oracle sparse assembly of Op(k) at n={W.n} + 1 Fourier-space apply + 1 K_P^-1 column "
-              f"+ one 3b-column Gram; k-point time modelled as assembly + {PAPER_ITERS_FCC_PC} iterations "
-              f"(PAPER.md:1199) x (b={W.nev + 5} applies + preconditioner solves + 2 Grams)")
+    cpu = dict(last)
+    cpu["value"] = value
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "k-points/s", "n_gpus": args.gpus,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * float(np.mean(times)),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": workload_config(W, args),
-            "cpu_baseline": {"value": value, "unit": "k-points/s", "cores": cores, "kind": "oracle", "sample": sample},
-            "e2e": {"value": value, "unit": "k-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-            "oracle_components": comps[-1] if comps else None}
+            "data": "synthetic", "config": workload_config(W, args), "cpu_baseline": cpu,
+            "e2e": {"value": value, "unit": "k-points/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
 
@@ -229,7 +325,12 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + ranks sharing GPUs (rank -> device rank %% count): a functional test of the "
                          "multi-rank path on a smaller box; numbers from it are not scaling results")
+    ap.add_argument("--oracle-worker", action="store_true", help=argparse.SUPPRESS)
+    ap.add_argument("--kidx", type=int, default=0, help=argparse.SUPPRESS)
+    ap.add_argument("--c2k", type=int, default=-1, help=argparse.SUPPRESS)
     args = ap.parse_args()
+    if args.oracle_worker:
+        return oracle_worker(args)
     if args.impl == "reference":
         return run_reference(args)
 
@@ -477,7 +578,8 @@ def main():
         pinned_masks = pin.numpy().reshape(masks.shape)
         nctx = len(ctxs)
 
-        def e2e_job(idx_list):
+        def e2e_job(svals):
+            idx_list = [kidx(s_) for s_ in svals]
             ce = [api.pc_create(A, W.n, eps1, pinned_masks, device=local) for _ in range(nctx)]
             for c_ in ce:
                 if args.guard is not None:
@@ -486,7 +588,7 @@ def main():
                     api.pc_set_option(c_, "w_guard", args.w_guard)
                 api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
             res = bands.band_structure(ce, kp, nev=W.nev, tol=args.tol, maxit=args.maxit, seed=0, device=cdev,
-                                       ks=sorted(set(idx_list)))
+                                       ks=sorted({kidx(s_, r) for r in range(world) for s_ in svals}))
             sel = np.array(idx_list, dtype=np.int64)
             out = (res["omega2"][sel], res["resid"][sel], res["iters"][sel], res["status"][sel])
             for c_ in ce:
@@ -495,13 +597,12 @@ def main():
 
         # one untimed job: steady state (the library caches the workspace of a destroyed context for
         # the next one on the device, see pc_destroy / pc_trim)
-        e2e_job([kidx(0)])
+        e2e_job([0])
         torch.cuda.synchronize()
         t0 = time.perf_counter()
         # the same k-points as the timed device steps (when e2e_steps == steps), so E and value differ only
         # by what the end-to-end path adds (uploads, context setup, host round trips)
-        eidx = [kidx(s) for s in range(nwarm, nwarm + args.e2e_steps)]
-        e_it = [int(v) for v in e2e_job(eidx)[2]]
+        e_it = [int(v) for v in e2e_job(range(nwarm, nwarm + args.e2e_steps))[2]]
         torch.cuda.synchronize()
         te = time.perf_counter() - t0
         tt = torch.tensor([te], dtype=torch.float64, device=cdev)
@@ -521,26 +622,17 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cores = len(os.sched_getaffinity(0))
-            _, tcomp = oracle_sample(W, kk, 1, masks=masks)
-            v, per_it = oracle_kpts_per_s(tcomp, PAPER_ITERS_FCC_PC)
-            cpu = {"value": v, "unit": "k-points/s", "cores": cores, "kind": "oracle",
-                   "sample": f"oracle sparse assembly at n={W.n} + 1 apply + 1 K_P^-1 column + one 3b-column Gram "
-                             f"timed; k-point modelled as assembly + {PAPER_ITERS_FCC_PC} iterations (PAPER.md:1199; "
-                             f"same model as --impl reference; this GPU run needed {np.mean(iters):.1f}) x "
-                             f"(b={W.nev + 5} applies+precond + 2 Grams) = "
-                             f"{tcomp['assembly_s']:.1f} s + {PAPER_ITERS_FCC_PC} x {per_it:.1f} s",
-                   "components": tcomp}
+            cpu = oracle_baseline(args, W, idx, with_c2=True)
         except Exception as ex:  # pragma: no cover
-            cpu = {"value": None, "error": str(ex)}
+            cpu = {"value": None, "error": str(ex)[:300]}
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": "k-points/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-                "config": workload_config(W, args) | {"kpoints_per_rank": args.steps,
-                                                      "parallelism": f"k-path sharded over {world} GPU(s), "
-                                                                     f"{len(ctxs)} concurrent k-point solve(s) per GPU"},
+                "config": workload_config(W, args), "kpoints_per_rank": args.steps,
+                "parallelism": f"k-path over {world} GPU(s) from one dynamic queue, {len(ctxs)} concurrent "
+                               f"k-point solve(s) per GPU, one all-gather",
                 "iters": iters, "status": status, "warmup_iters": wit, "alt_precond": alt,
                 "omega2_first_k": om[0].tolist(), "resid_max": float(rs.max()),
                 "apply": apply, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,

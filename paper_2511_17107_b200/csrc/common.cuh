@@ -3,7 +3,7 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <mutex>
-#include <set>
+#include <map>
 #include <utility>
 
 #define DEV __device__ __forceinline__
@@ -11,18 +11,20 @@
 
 typedef double2 cplx;
 
-// cudaFuncSetAttribute is a per-device setting: the dynamic shared-memory limit of `kern` is set once
-// per (kernel, current device).  (A process-wide "done" flag would leave the kernel without it on a
-// second device used by another context, and its launches would fail.)
+// cudaFuncSetAttribute is a per-device setting: the dynamic shared-memory limit of `kern` is raised to
+// `bytes` once per (kernel, current device) -- and again whenever a launch needs more than was set.
+// (A process-wide "done" flag would leave the kernel without it on a second device used by another
+// context, or below a later, larger request; such launches fail with cudaErrorInvalidValue.)
 inline cudaError_t smem_attr(const void* kern, int bytes) {
   static std::mutex mu;
-  static std::set<std::pair<const void*, int>> done;
+  static std::map<std::pair<const void*, int>, int> done;
   int dev = 0;
   cudaGetDevice(&dev);
   std::lock_guard<std::mutex> lk(mu);
-  if (done.count({kern, dev})) return cudaSuccess;
+  auto it = done.find({kern, dev});
+  if (it != done.end() && it->second >= bytes) return cudaSuccess;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (e == cudaSuccess) done.insert({kern, dev});
+  if (e == cudaSuccess) done[{kern, dev}] = bytes;
   return e;
 }
 

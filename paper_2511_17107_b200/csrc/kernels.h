@@ -54,6 +54,10 @@ cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out
 // launch_xex), x-forward DFT, y-forward DFT of every z-plane of every column, unnormalised, in -> out
 // (must differ).  One thread-block cluster of 8 CTAs per z-plane (distributed shared memory).
 bool plane_supported(int n);
+// second design (plane2.cu, N = 128): clusters of 16 CTAs (two per SM), exchange by remote stores
+bool plane2_supported(int n);
+cudaError_t launch_plane2(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
+                          const EpsCoef& ec, const cplx* tw, cudaStream_t st);
 cudaError_t launch_plane(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                          const EpsCoef& ec, const cplx* tw, cudaStream_t st);
 

@@ -601,10 +601,11 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
   const bool plane_local = c->fuse_xex && (op.mode != PC_EPS_CROSSDOF || (!op.ec->has[1] && !op.ec->has[2]));
   if (plane_local) {
-    if (c->plane_fuse && plane_supported(n)) {
-      // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane.cu)
+    if (c->plane_fuse && (c->plane_fuse == 2 ? plane2_supported(n) : plane_supported(n))) {
+      // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane.cu / plane2.cu)
       Prof p(c, PC_STAT_EPS, st, 1, 4 * fl + 100.0 * pts, 97.0 * pts);
-      cudaError_t e = launch_plane(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
+      cudaError_t e = (c->plane_fuse == 2) ? launch_plane2(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st)
+                                           : launch_plane(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
       if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("plane pass: ") + cudaGetErrorString(e));
     } else {
       // y-inverse, (x-inverse + M_eps + x-forward) fused, y-forward
@@ -910,7 +911,7 @@ extern "C" int pc_debug_heevj(const double* A_host, int n, double* w_host, doubl
 // Kernel timing entry for the LOBPCG block kernels on random data (tools/bench_block.py): the shapes
 // of one iteration with b X columns, na W columns and nP P columns on this context's grid.
 // which = 0: fused update (+ residual, K_P^{-1}); 1: Gram S^H [W P AW AP] (+ assembly); 2: Gram
-// S^H [W AW].  ms = mean milliseconds per launch group over reps (CUDA events on the context stream).
+// S^H [W AW]; 3: TMA update.  ms = mean milliseconds per launch group over reps (CUDA events on the context stream).
 extern "C" int pc_bench_block(pc_ctx* c, int which, int b, int na, int nP, int reps, double* ms) {
   if (!c || !ms || b < 1 || na < 0 || nP < 0 || nP > na || na > b || reps < 1)
     return set_err(PC_EINVAL, "pc_bench_block: bad arguments");

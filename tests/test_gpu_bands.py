@@ -37,24 +37,44 @@ def rel(a, b):
 
 
 def test_c1_vacuum_n8_golden(api):
-    """BASELINE config 1: SC vacuum n=8, 6 smallest vs closed form."""
+    """BASELINE config 1: SC vacuum n=8, 6 smallest vs closed form, from the default
+    (plane-wave) start and from a seeded Gaussian start, both at the parity tolerance 1e-7."""
     g = golden("c1_vacuum_n8.txt")
     ctx = api.pc_create(np.eye(3), 8, np.eye(3), np.zeros((4, 8, 8, 8), np.uint8))
-    # default (plane-wave) start; the Gaussian start at k_a, whose 6-fold cluster is cut by the block
-    # edge, is a known weak case of the non-orthogonalised basis at tol < 1e-5 (DESIGN.md)
-    r = api.pc_bands(ctx, [[PI, PI, PI], [PI / 7, 3 * PI / 5, 4 * PI / 13]], nev=6, tol=TOL)
+    kp = [[PI, PI, PI], [PI / 7, 3 * PI / 5, 4 * PI / 13]]
+    r = api.pc_bands(ctx, kp, nev=6, tol=TOL)
     assert (r["status"] == 0).all()
     assert rel(r["omega2"][0], g["k_a"]) <= 1e-8
     assert rel(r["omega2"][1], g["k_b"]) <= 1e-8
     api.pc_set_option(ctx, "start", 0)
-    r = api.pc_bands(ctx, [[PI, PI, PI], [PI / 7, 3 * PI / 5, 4 * PI / 13]], nev=6, tol=1e-5)
-    assert (r["status"] == 0).all()
-    assert rel(r["omega2"], np.stack([g["k_a"], g["k_b"]])) <= 1e-8
-    api.pc_set_option(ctx, "start", 1)
-    # pure transverse plane waves are the vacuum eigenvectors (P:370-373, 509-517): immediate convergence
+    for seed in (0, 7):
+        r = api.pc_bands(ctx, kp, nev=6, tol=TOL, seed=seed)
+        assert (r["status"] == 0).all()
+        assert rel(r["omega2"], np.stack([g["k_a"], g["k_b"]])) <= 1e-8
+
+
+def test_c1_vacuum_iterations(api):
+    """In vacuum K_P^{-1} is the exact inverse (M_eps = I), so the preconditioned Rayleigh
+    quotient is constant (Prop. P:550-569; "converges in <= 2 iterations").  Reading R17
+    (DESIGN.md): that holds for a start block inside the invariant subspace -- the transverse plane
+    waves, which are the vacuum eigenvectors, converge at once -- while from a
+    generic start T = A^{-1} makes LOBPCG an inverse iteration with Rayleigh-Ritz: the residual of band j
+    falls by at least lambda_j / lambda_{b+1} per step, which bounds the iteration count."""
+    g = golden("c1_vacuum_n8.txt")
+    ctx = api.pc_create(np.eye(3), 8, np.eye(3), np.zeros((4, 8, 8, 8), np.uint8))
+    kb = [PI / 7, 3 * PI / 5, 4 * PI / 13]
     api.pc_set_option(ctx, "start_noise", 0.0)
-    r = api.pc_bands(ctx, [[PI / 7, 3 * PI / 5, 4 * PI / 13]], nev=6, tol=TOL)
+    r = api.pc_bands(ctx, [kb], nev=6, tol=TOL)
     assert r["iters"].max() <= 2 and rel(r["omega2"][0], g["k_b"]) <= 1e-8
+    api.pc_set_option(ctx, "start", 0)
+    b = 6 + 6
+    lam = _vacuum_closed(8, np.array(kb), np.eye(3), b + 1, O.gamma_rule(kb))
+    rate = lam[5] / lam[b]
+    res0 = 1e5  # >= ||A|| x relative admixture of a unit Gaussian start at n = 8 (gamma max|kappa|^2 ~ 3e4)
+    bound = int(np.ceil(np.log(TOL / res0) / np.log(rate))) + 2
+    r = api.pc_bands(ctx, [kb], nev=6, tol=TOL, seed=3)
+    assert r["status"][0] == 0 and rel(r["omega2"][0], g["k_b"]) <= 1e-8
+    assert r["iters"][0] <= bound, (r["iters"][0], bound, rate)
 
 
 def test_homogeneous_n8_golden(api):

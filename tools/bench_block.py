@@ -40,4 +40,6 @@ for w in a.which:
     else:
         cols = p + a.na
     out[w] = {"ms": round(ms, 4), "gbs": round(16.0 * rows * cols / ms / 1e6, 1), "cols": cols}
+    if w == 1:  # algorithmic Gram flops: p x 2c complex MACs per row, 8 flops each
+        out[w]["alg_tflops"] = round(8.0 * rows * p * 2 * (a.na + a.np) / ms / 1e9, 2)
 print(json.dumps(out))
