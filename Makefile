@@ -8,7 +8,7 @@ BUILD     := build
 LIB       := paper_2511_17107_b200/libpcband.so
 FFT_N     := 4 6 8 10 12 16 20 24 32 40 48 64 80 96 100 120 128 160 192 240 256
 FFT_OBJS  := $(foreach n,$(FFT_N),$(BUILD)/fft_$(n).o)
-OBJS      := $(FFT_OBJS) $(BUILD)/dispatch.o $(BUILD)/pointwise.o $(BUILD)/blas.o $(BUILD)/update_all.o $(BUILD)/update_tmap.o $(BUILD)/gram.o $(BUILD)/plane.o $(BUILD)/plane2.o $(BUILD)/rr.o $(BUILD)/pcband.o
+OBJS      := $(FFT_OBJS) $(BUILD)/dispatch.o $(BUILD)/pointwise.o $(BUILD)/blas.o $(BUILD)/update_all.o $(BUILD)/update_tmap.o $(BUILD)/gram.o $(BUILD)/plane2.o $(BUILD)/rr.o $(BUILD)/pcband.o
 HDRS      := $(wildcard $(SRC)/*.cuh $(SRC)/*.h) include/pcband.h
 
 all: $(LIB)

@@ -165,7 +165,10 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "guard"        extra LOBPCG block columns beyond nev (default 6)
  *   "apply_chunk"  max columns per batched apply (default 0 = all at once)
  *   "profile"      1: time every kernel class with CUDA events (read with pc_stats), 0: off
- *   "drop_tol"     Rayleigh-Ritz rank threshold on the scaled Gram eigenvalues (default 1e-12)
+ *   "drop_tol"     Rayleigh-Ritz rank threshold on the Jacobi-scaled mass Gram: Cholesky pivots / SVQB
+ *                  eigenvalues below it (relative) are dropped and P restarts (default 1e-8; at 1e-12
+ *                  an ill-conditioned basis let the Ritz coefficients grow and the solve diverge on
+ *                  degenerate vacuum clusters from a Gaussian start)
  *   "kindex_offset" global index of kpts[0] in pc_bands (start-block seeds are keyed by it, so
  *                  results do not depend on how a k-path is split across GPUs; default 0)
  *   "start"        0: Gaussian start block; 1 (default): transverse plane waves of the b/2 modes
@@ -194,8 +197,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *   "fuse_xex"     1 (default): fused x-DFT + M_eps + x-DFT pass when eps_13 = eps_23 = 0 (or
  *                  Diagonal/Trivial mode); 0: 7-pass pipeline with the standalone stencil
  *   "plane_fuse"   1: at n = 128 the y-inverse, x-inverse + M_eps + x-forward and y-forward passes of
- *                  a z-plane-local medium run as one pass over thread-block clusters of 8 CTAs
- *                  (plane.cu: 3 HBM passes per apply instead of 5; measured slower: 3.14 vs 1.98 ms
+ *                  a z-plane-local medium run as one pass over thread-block clusters of 16 CTAs
+ *                  (plane2.cu: 3 HBM passes per apply instead of 5; measured slower: 2.67 vs 1.93 ms
  *                  per 15 columns); 0 (default): the three passes
  *   "fuse_resid"   1 (default): both block updates + next residual + K_P^{-1} in one pass; 0: two
  *                  update launches and a separate residual pass

@@ -50,16 +50,12 @@ cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& i
 cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                        const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st);
 
-// fused xy-plane pass (plane.cu, N = 128): y-inverse DFT, x-inverse DFT, M_eps (same media as
+// fused xy-plane pass (plane2.cu, N = 128): y-inverse DFT, x-inverse DFT, M_eps (same media as
 // launch_xex), x-forward DFT, y-forward DFT of every z-plane of every column, unnormalised, in -> out
-// (must differ).  One thread-block cluster of 8 CTAs per z-plane (distributed shared memory).
-bool plane_supported(int n);
-// second design (plane2.cu, N = 128): clusters of 16 CTAs (two per SM), exchange by remote stores
+// (must differ).  One thread-block cluster of 16 CTAs per z-plane (distributed shared memory).
 bool plane2_supported(int n);
 cudaError_t launch_plane2(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                           const EpsCoef& ec, const cplx* tw, cudaStream_t st);
-cudaError_t launch_plane(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
-                         const EpsCoef& ec, const cplx* tw, cudaStream_t st);
 
 // pointwise ---------------------------------------------------------------------------------
 void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t st);

@@ -142,14 +142,14 @@ struct pc_ctx {
   DevBuf kxws;        // apply workspace: gamma (kappa . xhat), N^3 per column (first pass -> last pass)
   int apply_chunk = 0;
   int guard = 6;  // block b = nev + guard (reading R14; measured optimum of the current kernels)
-  double drop_tol = 1e-12;
+  double drop_tol = 1e-8;   // Rayleigh-Ritz rank threshold (scaled mass Gram); see DESIGN R14
   long long kindex_offset = 0;  // global index of kpts[0] (seeds independent of sharding)
   int verbose = 0;
   int p_restart = 1;  // drop the P block when the Rayleigh-Ritz basis is rank deficient
   int sticky_lock = 0;         // 1: locked columns stay locked (SciPy's activeMask &=); 0: may re-activate
   int gram_refresh = 16;       // every n-th iteration uses the full Gram (no X^H X = I assumption)
   int fuse_xex = 1;            // fused x-DFT + M_eps + x-DFT pass for z-plane-local media
-  int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane.cu; measured slower)
+  int plane_fuse = 0;          // 1, n = 128: one cluster pass for y/x DFTs + M_eps (plane2.cu; measured slower)
   int w_guard = 0;             // >= 0: only the first nev + w_guard columns get W; -1: all b columns
   int precond = 0;             // 0: K_P^{-1}; 1: eps-weighted K_P^{-1} (beyond the paper, see precond_eps)
   int precond_fuse = 1;        // precond = 1 in pc_bands: its last pass and the apply's first pass as one (OP_KAGH)
@@ -601,11 +601,10 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
   const bool plane_local = c->fuse_xex && (op.mode != PC_EPS_CROSSDOF || (!op.ec->has[1] && !op.ec->has[2]));
   if (plane_local) {
-    if (c->plane_fuse && (c->plane_fuse == 2 ? plane2_supported(n) : plane_supported(n))) {
-      // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane.cu / plane2.cu)
+    if (c->plane_fuse && plane2_supported(n)) {
+      // one HBM round trip for y-inverse, x-inverse, M_eps, x-forward, y-forward (plane2.cu)
       Prof p(c, PC_STAT_EPS, st, 1, 4 * fl + 100.0 * pts, 97.0 * pts);
-      cudaError_t e = (c->plane_fuse == 2) ? launch_plane2(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st)
-                                           : launch_plane(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
+      cudaError_t e = launch_plane2(n, op.mode, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, st);
       if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("plane pass: ") + cudaGetErrorString(e));
     } else {
       // y-inverse, (x-inverse + M_eps + x-forward) fused, y-forward

@@ -1,4 +1,4 @@
-// Fused xy-plane pass of pc_apply at N = 128, second design (option plane_fuse = 2): one HBM round
+// Fused xy-plane pass of pc_apply at N = 128, option plane_fuse = 1: one HBM round
 // trip for the middle factor F_y F_x M_eps F_x^H F_y^H of Op in Fourier coordinates (
 // M_eps of P:607-673, readings R4/R5) for media whose eps_1 couples only E^1 and E^2 (eps_13 = eps_23
 // = 0, or Diagonal / Trivial mode).  Replaces the y-inverse pass, the fused x/M_eps/x pass and the
@@ -7,8 +7,8 @@
 //
 // One z-plane of one column (3 x 128 x 128 complex, 786 KB) is spread over a cluster of 16 CTAs of
 // 108 KB shared memory each, so that two CTAs (of different planes) share an SM and one's HBM phases
-// overlap the other's DFT phases (the 8-CTA design of plane.cu ran one 214-KB CTA per SM, its phases
-// serialised).  CTA q owns the x-slab x in [8q, 8q+8) and the y-rows [8q, 8q+8):
+// overlap the other's DFT phases (a round-1 8-CTA design with one 214-KB CTA per SM, its phases serialised,
+// took 3.14 ms per 15 columns).  CTA q owns the x-slab x in [8q, 8q+8) and the y-rows [8q, 8q+8):
 //   1. y-inverse DFT of its x-slab: the radix-16 first step reads HBM straight into registers (8 lanes
 //      = one 128-B row segment), mid layout in Ty; the radix-8 second step PUSHES each output (c, y, x)
 //      into the Tx row block of the CTA owning row y (distributed shared memory stores, 128-B runs),
@@ -17,6 +17,10 @@
 //      whose second step pushes each output (c, y, x) into the Ty slab of the CTA owning column x.
 //   3. cluster barrier; y-forward DFT, the second step writes HBM directly.
 // No CTA reads another's shared memory: all exchange is by remote stores before a cluster barrier.
+// Measured (C4, 15 columns): 2.67 ms against 1.93 ms for the y / xex / y passes it replaces; ncu: barrier
+// stalls lead (3.8 per issue), 21 % warps active, FP64 pipe 22 %, DRAM 1.1 TB/s -- every CTA runs its
+// load, DFT, exchange and store phases in sequence between two cluster barriers, and two CTAs per SM
+// do not hide that.  Kept as the 3-pass candidate (option plane_fuse, default off).
 // DFTs: 128 = 16 x 8 two-step Stockham with the register codelets of dft.cuh, twiddles from a
 // transposed shared table (xex.cuh).  Unnormalised, as the passes it replaces.
 #include <cooperative_groups.h>
