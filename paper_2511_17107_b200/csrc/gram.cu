@@ -225,7 +225,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
                  cudaStream_t st) {
   struct Opt { int bm, bn; };
   const Opt opts[] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}, {40, 40}, {40, 64}, {64, 64}, {80, 64},
-                      {80, 96}, {24, 32}, {48, 96}, {40, 24}};
+                      {80, 96}, {24, 32}, {48, 96}, {40, 24}, {24, 8}, {40, 8}, {24, 16}, {40, 16}};
   const int nopt = sizeof(opts) / sizeof(opts[0]);
   int best = 0;
   double best_cost = 1e300;
@@ -258,6 +258,12 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     case 8: PC_GRAM_CASE(5, 3, 2, 4, 16, 2) break;
     case 9: PC_GRAM_CASE(3, 1, 1, 4, 16, 3) break;
     case 11: PC_GRAM_CASE(5, 1, 1, 3, 16, 3) break;
+    // narrow T blocks (few active W/P columns in the tail of a solve): one or two 8-column warp tiles,
+    // so the row chunks are split over 4 (2) warp groups instead
+    case 12: run_gram<3, 1, 1, 1, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;
+    case 13: run_gram<5, 1, 1, 1, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;
+    case 14: run_gram<3, 1, 1, 2, 16, 3, 2>(S, p, T, q, len, G, partial, st); break;
+    case 15: run_gram<5, 1, 1, 2, 16, 3, 2>(S, p, T, q, len, G, partial, st); break;
     default: PC_GRAM_CASE(3, 3, 2, 4, 16, 3) break;
   }
 }
