@@ -325,6 +325,8 @@ def main():
     ap.add_argument("--dist-backend", default="nccl", choices=["nccl", "gloo"],
                     help="gloo + ranks sharing GPUs (rank -> device rank %% count): a functional test of the "
                          "multi-rank path on a smaller box; numbers from it are not scaling results")
+    ap.add_argument("--cpu-c2", action="store_true",
+                    help="cpu_baseline also runs complete oracle solves of C2 path points (1-2 min more)")
     ap.add_argument("--oracle-worker", action="store_true", help=argparse.SUPPRESS)
     ap.add_argument("--kidx", type=int, default=0, help=argparse.SUPPRESS)
     ap.add_argument("--c2k", type=int, default=-1, help=argparse.SUPPRESS)
@@ -622,7 +624,7 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            cpu = oracle_baseline(args, W, idx, with_c2=True)
+            cpu = oracle_baseline(args, W, idx, with_c2=args.cpu_c2)
         except Exception as ex:  # pragma: no cover
             cpu = {"value": None, "error": str(ex)[:300]}
 

@@ -1,4 +1,7 @@
-"""Per-pass CUDA-event times of one 15-column pc_apply at the bench workload (C4, n=128)."""
+"""Per-pass CUDA-event times of one 15-column pc_apply at the bench workload (C4, n=128).
+
+usage: python tools/apply_time.py [C4] [ncols] [key=value ...]   (eps=sdd: the general eps_1 with all three
+       off-diagonal couplings, which runs the 7-pass path with the standalone stencil)"""
 import json
 import os
 import sys
@@ -13,9 +16,10 @@ W = synth.WORKLOADS[sys.argv[1] if len(sys.argv) > 1 else "C4"]
 ncol = int(sys.argv[2]) if len(sys.argv) > 2 else 15
 A = W.A()
 masks = synth.make_masks(W.geometry, A, W.n)
-ctx = api.pc_create(A, W.n, W.eps1(), masks)
-for kv in sys.argv[3:]:  # extra key=value options
-    key, v = kv.split("=")
+opts = dict(kv.split("=") for kv in sys.argv[3:])  # extra key=value options
+eps1 = synth.eps_sdd() if opts.pop("eps", "") == "sdd" else W.eps1()
+ctx = api.pc_create(A, W.n, eps1, masks)
+for key, v in opts.items():
     api.pc_set_option(ctx, key, float(v))
 X = torch.randn(ncol, 3 * W.n ** 3, dtype=torch.complex128, device="cuda")
 Y = torch.empty_like(X)
@@ -34,6 +38,7 @@ torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / reps
 st = api.pc_stats(ctx)
 pts = W.n ** 3 * ncol
-out = {"ms": ms, "alg_gbs": 336 * pts / ms / 1e6, "design_gbs": 513 * pts / ms / 1e6,
+design = sum(v["bytes"] for v in st.values() if isinstance(v, dict)) / reps / pts  # B per point per column
+out = {"ms": ms, "alg_gbs": 336 * pts / ms / 1e6, "design_bytes_per_point": design, "design_gbs": design * pts / ms / 1e6,
        "classes": {k_: round(v["ms"] / reps, 4) for k_, v in st.items() if isinstance(v, dict) and v["count"]}}
 print(json.dumps(out))
