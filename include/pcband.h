@@ -154,6 +154,23 @@ int pc_bands(pc_ctx *ctx, const double *kpts, int nk, int nev, double tol, int m
              unsigned long long seed, double *omega2, double *resid, int *iters, int *status,
              void *evecs);
 
+/*
+ * pc_apply_multi / pc_precond_multi — several Bloch vectors in ONE launch (k as an
+ * extra column dimension; at n <= 64 one k-point's block under-fills 148 SMs).  Column j of X / R is
+ * processed with k = kpts[3*kcol[j] .. 3*kcol[j]+2]: pc_apply_multi computes Y_j = Op(k) X_j in Fourier
+ * coordinates exactly as pc_apply (PC_SPACE_FOURIER), pc_precond_multi P_j = K_P(k)^{-1} R_j as
+ * pc_precond (the paper's K_P^{-1}, whatever option "precond" says).  Per-k symbol tables,
+ * penalties gamma(k) and pass-through thresholds (reading R7) live in a context buffer.
+ *   kpts  host, nk*3 Cartesian Bloch vectors, 1 <= nk <= 16
+ *   kcol  host, ncols ints in [0, nk)
+ *   X, Y, R, P, ncols, ld, stream: as pc_apply / pc_precond.
+ * Returns PC_EINVAL for nk out of range, a k index out of range, null pointers or aliasing X == Y.
+ */
+int pc_apply_multi(pc_ctx *ctx, const double *kpts, int nk, const int *kcol, const void *X, void *Y, int ncols,
+                   long long ld, void *stream);
+int pc_precond_multi(pc_ctx *ctx, const double *kpts, int nk, const int *kcol, const void *R, void *P, int ncols,
+                     long long ld, void *stream);
+
 /* Penalty gamma used for k (override if set, else P:457-462). */
 double pc_gamma(const pc_ctx *ctx, const double k[3]);
 

@@ -49,6 +49,8 @@ def lib():
         "pc_create": (i, [ctypes.POINTER(vp), dp, i, dp, ctypes.POINTER(ctypes.c_uint8), i, d, i]),
         "pc_apply": (i, [vp, dp, vp, vp, i, ll, i, vp]),
         "pc_precond": (i, [vp, dp, vp, vp, i, ll, vp]),
+        "pc_apply_multi": (i, [vp, dp, i, ip, vp, vp, i, ll, vp]),
+        "pc_precond_multi": (i, [vp, dp, i, ip, vp, vp, i, ll, vp]),
         "pc_apply_eps": (i, [vp, vp, vp, i, ll, vp]),
         "pc_fft3": (i, [vp, vp, vp, i, ll, i, vp]),
         "pc_bands": (i, [vp, dp, i, i, d, i, ull, dp, dp, ip, ip, vp]),
@@ -92,17 +94,35 @@ def _stream_ptr(stream):
     return ctypes.c_void_p(stream.cuda_stream)
 
 
-def _block(t, ncols=None):
-    """(pointer, ncols, ld) of a torch complex128 CUDA block (ncols, >= 3N^3)."""
+def _block(t, ctx=None):
+    """(pointer, ncols, ld) of a torch complex128 CUDA block (ncols, >= 3N^3): contiguous columns, column
+    stride >= column length (no expanded/overlapping views), and, given ctx, columns of >= 3N^3."""
     import torch
     if not (isinstance(t, torch.Tensor) and t.is_cuda and t.dtype == torch.complex128):
         raise PcError(PC_EINVAL, "device blocks must be CUDA complex128 torch tensors")
     if t.dim() == 1:
         t = t.unsqueeze(0)
-    if t.stride(-1) != 1:
-        raise PcError(PC_EINVAL, "block columns must be contiguous")
-    nc = t.shape[0] if ncols is None else ncols
-    return ctypes.c_void_p(t.data_ptr()), nc, max(t.stride(0), t.shape[-1])
+    if t.dim() != 2 or t.stride(-1) != 1:
+        raise PcError(PC_EINVAL, "a block is (ncols, len) with contiguous columns")
+    nc = t.shape[0]
+    ld = t.stride(0) if nc > 1 else t.shape[-1]
+    if ld < t.shape[-1]:
+        raise PcError(PC_EINVAL, "column stride smaller than the column length (expanded or overlapping view)")
+    if ctx is not None and t.shape[-1] < ctx.len:
+        raise PcError(PC_EINVAL, f"columns hold {t.shape[-1]} < 3 N^3 = {ctx.len} values")
+    return ctypes.c_void_p(t.data_ptr()), nc, ld
+
+
+def _pair(ctx, X, Y, same_ld=True):
+    """Input/output blocks of one call: equal leading dimension (the ABI has one ld), output at least as
+    many columns as the input."""
+    px, nc, ld = _block(X, ctx)
+    py, ncy, ldy = _block(Y, ctx)
+    if ncy < nc:
+        raise PcError(PC_EINVAL, f"output block has {ncy} < {nc} columns")
+    if nc > 1 and ldy != ld:
+        raise PcError(PC_EINVAL, "input and output blocks must share the leading dimension")
+    return px, py, nc, ld
 
 
 class Ctx:
@@ -152,29 +172,47 @@ def pc_create(A, n, eps1, masks, eps_mode="crossdof", gamma_override=0.0, device
 
 def pc_apply(ctx: Ctx, k, X, Y, space=PC_SPACE_FOURIER, stream=None):
     kk = np.ascontiguousarray(np.asarray(k, dtype=np.float64).reshape(3))
-    px, nc, ld = _block(X)
-    py, _, ldy = _block(Y)
-    if ldy != ld:
-        raise PcError(PC_EINVAL, "X and Y must share the leading dimension")
+    px, py, nc, ld = _pair(ctx, X, Y)
     _check(lib().pc_apply(ctx.h, _dptr(kk), px, py, nc, ld, int(space), _stream_ptr(stream)))
 
 
 def pc_precond(ctx: Ctx, k, R, P, stream=None):
     kk = np.ascontiguousarray(np.asarray(k, dtype=np.float64).reshape(3))
-    pr, nc, ld = _block(R)
-    pp, _, _ = _block(P)
+    pr, pp, nc, ld = _pair(ctx, R, P)
     _check(lib().pc_precond(ctx.h, _dptr(kk), pr, pp, nc, ld, _stream_ptr(stream)))
 
 
+def _multik(kpts, kcol, ncols):
+    kk = np.ascontiguousarray(np.asarray(kpts, dtype=np.float64).reshape(-1, 3))
+    kc = np.ascontiguousarray(np.asarray(kcol, dtype=np.int32).reshape(-1))
+    if kc.size < ncols:
+        raise PcError(PC_EINVAL, "kcol needs one k index per column")
+    return kk, kc
+
+
+def pc_apply_multi(ctx: Ctx, kpts, kcol, X, Y, stream=None):
+    """Y[j] = Op(kpts[kcol[j]]) X[j] for every column j, one launch sequence for all k (Fourier space)."""
+    px, py, nc, ld = _pair(ctx, X, Y)
+    kk, kc = _multik(kpts, kcol, nc)
+    _check(lib().pc_apply_multi(ctx.h, _dptr(kk), kk.shape[0], kc.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                px, py, nc, ld, _stream_ptr(stream)))
+
+
+def pc_precond_multi(ctx: Ctx, kpts, kcol, R, P, stream=None):
+    """P[j] = K_P(kpts[kcol[j]])^{-1} R[j] for every column j (Fourier space)."""
+    pr, pp, nc, ld = _pair(ctx, R, P)
+    kk, kc = _multik(kpts, kcol, nc)
+    _check(lib().pc_precond_multi(ctx.h, _dptr(kk), kk.shape[0], kc.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
+                                  pr, pp, nc, ld, _stream_ptr(stream)))
+
+
 def pc_apply_eps(ctx: Ctx, E, Y, stream=None):
-    pe, nc, ld = _block(E)
-    py, _, _ = _block(Y)
+    pe, py, nc, ld = _pair(ctx, E, Y)
     _check(lib().pc_apply_eps(ctx.h, pe, py, nc, ld, _stream_ptr(stream)))
 
 
 def pc_fft3(ctx: Ctx, X, Y, direction=PC_FFT_TO_FOURIER, stream=None):
-    px, nc, ld = _block(X)
-    py, _, _ = _block(Y)
+    px, py, nc, ld = _pair(ctx, X, Y)
     _check(lib().pc_fft3(ctx.h, px, py, nc, ld, int(direction), _stream_ptr(stream)))
 
 
@@ -186,7 +224,14 @@ def pc_bands(ctx: Ctx, kpts, nev, tol=1e-5, maxit=500, seed=0, evecs=None, allow
     rs = np.zeros((nk, nev))
     it = np.zeros(nk, dtype=np.int32)
     stt = np.zeros(nk, dtype=np.int32)
-    ev = ctypes.c_void_p(evecs.data_ptr()) if evecs is not None else None
+    ev = None
+    if evecs is not None:
+        import torch
+        need = nk * nev * ctx.len
+        if not (isinstance(evecs, torch.Tensor) and evecs.is_cuda and evecs.dtype == torch.complex128
+                and evecs.is_contiguous() and evecs.numel() >= need):
+            raise PcError(PC_EINVAL, f"evecs must be a contiguous CUDA complex128 tensor of >= {need} elements")
+        ev = ctypes.c_void_p(evecs.data_ptr())
     allow = (PC_OK, PC_ENOTCONV) if allow_notconv else (PC_OK,)
     rc = _check(lib().pc_bands(ctx.h, _dptr(k), nk, int(nev), float(tol), int(maxit), int(seed), _dptr(om), _dptr(rs),
                                it.ctypes.data_as(ctypes.POINTER(ctypes.c_int)),
@@ -245,9 +290,8 @@ def pc_debug_pass(ctx: Ctx, k, kind, axis, direction, X, Y, XH=None, scale=1.0):
     """One FFT pass (test/tuning entry): kind 0 plain, 1 K_A^H-fused inverse z, 2 K_A + gamma K_B forward z
     (XH = the apply input x_hat).  Runs on the legacy default stream and synchronises."""
     kk = np.ascontiguousarray(np.asarray(k, dtype=np.float64).reshape(3))
-    px, nc, ld = _block(X)
-    py, _, _ = _block(Y)
-    pxh = _block(XH)[0] if XH is not None else None
+    px, py, nc, ld = _pair(ctx, X, Y)
+    pxh = _block(XH, ctx)[0] if XH is not None else None
     _check(lib().pc_debug_pass(ctx.h, _dptr(kk), int(kind), int(axis), int(direction), px, py, pxh, nc, ld,
                                float(scale)))
 

@@ -164,8 +164,15 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
   };
 
   for (int j = tid; j < N; j += NT) tw[j] = ldg(a.tw + j);
+  // symbol table of a column (multi-k launches: per-column k)
+  auto ktab_of = [&](int col) { return a.mk.on ? a.ktab + (size_t)a.mk.kcol[col] * 9 * N : a.ktab; };
+  int kt_col = -1;  // column whose z-pieces are in ktz
   if constexpr (C == 3) {
-    for (int e = tid; e < 3 * N; e += NT) cp_async16(&ktz[e], a.ktab + (3 * (e / N) + 2) * N + e % N);
+    if (blockIdx.x < ntiles) {
+      kt_col = (int)blockIdx.x / TPV;
+      const cplx* kt0 = ktab_of(kt_col);
+      for (int e = tid; e < 3 * N; e += NT) cp_async16(&ktz[e], kt0 + (3 * (e / N) + 2) * N + e % N);
+    }
   }
   int t = blockIdx.x;
   if (t < ntiles) load_tile(t, stage_base);
@@ -178,11 +185,26 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
     // symbol passes: the (x, y) pieces of kappa are per-thread constants (see the prologue); their loads
     // are issued before the tile wait so the latency overlaps it
     cplx kxy[3];
+    const cplx* kt = a.ktab;
+    double gam = a.gamma, thr = a.thr;
     if constexpr (C == 3) {
+      const int tcol = t / TPV;
+      kt = ktab_of(tcol);
+      if (a.mk.on) {
+        gam = a.mk.gamma[a.mk.kcol[tcol]];
+        thr = a.mk.thr[a.mk.kcol[tcol]];
+        if (tcol != kt_col) {  // persistent CTA moved to another column's tile: its k's z-pieces
+          __syncthreads();
+          for (int e = tid; e < 3 * N; e += NT) cp_async16(&ktz[e], kt + (3 * (e / N) + 2) * N + e % N);
+          cp_async_commit();
+          cp_async_wait<0>();
+          kt_col = tcol;
+        }
+      }
       int m1, m2, m3;
       tm.modes(0, tid % TP, m1, m2, m3);
 #pragma unroll
-      for (int i = 0; i < 3; i++) kxy[i] = ldg(a.ktab + 3 * i * N + m1) + ldg(a.ktab + (3 * i + 1) * N + m2);
+      for (int i = 0; i < 3; i++) kxy[i] = ldg(kt + 3 * i * N + m1) + ldg(kt + (3 * i + 1) * N + m2);
     }
 #if PC_KAG_PREFETCH
     // OP_KAG: the penalty scalars g of this thread's elements are loaded before the DFTs (registers),
@@ -222,7 +244,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
         cplx u3 = cmul(x1, conjg(k2)) - cmul(x2, conjg(k1));
         // kappa . xhat (no conjugation: K_B = conj(kappa) kappa^T), kept for the last pass
         const cplx kx = cmul(k1, x1) + cmul(k2, x2) + cmul(k3, x3);
-        gkx[tm.off(j, p)] = a.gamma * kx;
+        gkx[tm.off(j, p)] = gam * kx;
         s[SI(0, j, p)] = a.scale * u1;
         s[SI(1, j, p)] = a.scale * u2;
         s[SI(2, j, p)] = a.scale * u3;
@@ -281,7 +303,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
         const cplx k1 = kxy[0] + ktz[j], k2 = kxy[1] + ktz[N + j], k3 = kxy[2] + ktz[2 * N + j];
         const cplx s1 = s[SI(0, j, p)], s2 = s[SI(1, j, p)], s3 = s[SI(2, j, p)];
         const double kk = k1.x * k1.x + k1.y * k1.y + k2.x * k2.x + k2.y * k2.y + k3.x * k3.x + k3.y * k3.y;
-        const double inv = (kk > a.thr) ? 1.0 / kk : 0.0;
+        const double inv = (kk > thr) ? 1.0 / kk : 0.0;
         const cplx w1 = inv * (cmul(k2, s3) - cmul(k3, s2) + cmul(conjg(k1), g[q]));
         const cplx w2 = inv * (cmul(k3, s1) - cmul(k1, s3) + cmul(conjg(k2), g[q]));
         const cplx w3 = inv * (cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), g[q]));
@@ -324,7 +346,7 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
         cplx y3 = cmul(k1, s2) - cmul(k2, s1) + cmul(conjg(k3), g[q]);
         if (a.kscale) {
           const double kk = k1.x * k1.x + k1.y * k1.y + k2.x * k2.x + k2.y * k2.y + k3.x * k3.x + k3.y * k3.y;
-          const double inv = (kk > a.thr) ? 1.0 / kk : 0.0;
+          const double inv = (kk > thr) ? 1.0 / kk : 0.0;
           y1 = inv * y1;
           y2 = inv * y2;
           y3 = inv * y3;

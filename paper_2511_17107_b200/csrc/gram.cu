@@ -257,7 +257,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     case 7: PC_GRAM_CASE(5, 2, 2, 4, 16, 3) break;
     case 8: PC_GRAM_CASE(5, 3, 2, 4, 16, 2) break;
     case 9: PC_GRAM_CASE(3, 1, 1, 4, 16, 3) break;
-    case 11: PC_GRAM_CASE(5, 1, 1, 3, 16, 3) break;
+    case 11: run_gram<5, 1, 1, 3, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;
     // narrow T blocks (few active W/P columns in the tail of a solve): one or two 8-column warp tiles,
     // so the row chunks are split over 4 (2) warp groups instead
     case 12: run_gram<3, 1, 1, 1, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;

@@ -23,15 +23,26 @@ struct EpsCoef {
   int has[3];   // which off-diagonals are non-zero
 };
 
+#define PC_MAXK 16  // Bloch vectors per multi-k launch (pc_apply_multi / pc_precond_multi)
+
+// Several k-points in one launch: column j uses the symbol table ktab + kcol[j] * 9N and the
+// penalty / pass-through threshold of its k.
+struct MultiK {
+  int on = 0;
+  unsigned char kcol[PC_MAXCOLS];
+  double gamma[PC_MAXK], thr[PC_MAXK];
+};
+
 struct PassArgsH {
   const cplx* tw;    // tw[j] = exp(-2 pi i j / N)
-  const cplx* ktab;  // symbol pieces, see pointwise.cu
+  const cplx* ktab;  // symbol pieces, see pointwise.cu (multik: PC_MAXK consecutive 9N tables)
   double gamma;
   double scale;
   int z0 = 0, nz = 0;  // x/y passes: restrict to z-planes [z0, z0+nz) (nz = 0: all)
   double gamma2 = 0.0; // OP_KAGH: gamma of the apply that follows the preconditioner
   int kscale = 0;      // OP_KAG: output scaled by 1/|kappa|^2 per mode (0 where |kappa|^2 <= thr): the
   double thr = 0.0;    // last pass of the eps-weighted preconditioner (pcband.cu, precond_eps)
+  MultiK mk;           // mk.on: per-column k (ktab, gamma, thr of k index mk.kcol[col])
 };
 
 // Persistent grids: 148 SMs x resident CTAs per SM.
@@ -60,7 +71,7 @@ cudaError_t launch_plane2(int n, int mode, const ColPtrs& in, const MutColPtrs& 
 // pointwise ---------------------------------------------------------------------------------
 void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t st);
 void launch_precond(const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const cplx* kt, double gamma,
-                    double thr, cudaStream_t st);
+                    double thr, cudaStream_t st, const MultiK* mk = nullptr);
 void launch_eps(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const uint8_t* mask,
                 const EpsCoef& ec, cudaStream_t st);
 int resid_grid(int n);

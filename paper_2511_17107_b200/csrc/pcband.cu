@@ -167,6 +167,7 @@ struct pc_ctx {
   int warm_start = 0;          // 1: start from the previous k-point's Ritz vectors (same context, k != 0)
   int have_prev = 0, prev_slot = 0, prev_b = 0;
   DevBuf pwbuf;
+  DevBuf mkbuf;  // symbol tables of a multi-k launch (PC_MAXK x 9N)
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
@@ -418,6 +419,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   c->small.release();
   c->gpart.release();
   c->pwbuf.release();
+  c->mkbuf.release();
   auto t3 = now();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   auto t4 = now();
@@ -515,15 +517,8 @@ extern "C" int pc_stats(pc_ctx* c, double* out, int reset) {
 // ------------------------------------------------------------------------------------------
 // symbols for k (stream-ordered; cached while k is unchanged)
 // ------------------------------------------------------------------------------------------
-static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
-  c->cur_gamma = gamma_rule(c, k);
-  if (k[0] == c->cur_k[0] && k[1] == c->cur_k[1] && k[2] == c->cur_k[2]) return;
-  Sym3 s;
-  std::memcpy(s.B, c->B, sizeof(s.B));
-  for (int i = 0; i < 3; i++) s.k[i] = k[i];
-  c->launches += 1;
-  launch_ktab(c->d_ktab, c->d_tw, c->n, s, st);
-  // |kappa|^2 <= 1e-28 max|kappa|^2 -> pass-through (reading R7); max bounded via the 1-D pieces
+// |kappa|^2 <= 1e-28 max|kappa|^2 -> pass-through (reading R7); max bounded via the 1-D pieces
+static double pass_threshold(const pc_ctx* c, const double k[3]) {
   double bound = 0;
   const double n = c->n;
   for (int i = 0; i < 3; i++) {
@@ -532,7 +527,43 @@ static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
     m += std::fabs(k[i]);
     bound += m * m;
   }
-  c->cur_thr = 1e-28 * bound;
+  return 1e-28 * bound;
+}
+
+// Symbol tables of nk Bloch vectors for one multi-k launch: mkbuf holds nk consecutive 9N
+// tables, mk the per-k penalty and pass-through threshold; kcol (ncols entries) maps columns to k.
+static int build_multik(pc_ctx* c, const double* kpts, int nk, const int* kcol, int ncols, MultiK& mk,
+                        cudaStream_t st) {
+  if (nk < 1 || nk > PC_MAXK) return set_err(PC_EINVAL, "multi-k: 1 <= nk <= 16");
+  for (int j = 0; j < ncols; j++)
+    if (kcol[j] < 0 || kcol[j] >= nk) return set_err(PC_EINVAL, "multi-k: k index out of range");
+  const size_t tb = (size_t)9 * c->n * sizeof(cplx);
+  if ((size_t)nk * tb > c->mkbuf.bytes) {
+    cudaStreamSynchronize(st);
+    CHK(c->mkbuf.ensure((size_t)PC_MAXK * tb));
+  }
+  mk.on = 1;
+  for (int i = 0; i < nk; i++) {
+    Sym3 s;
+    std::memcpy(s.B, c->B, sizeof(s.B));
+    for (int a = 0; a < 3; a++) s.k[a] = kpts[3 * i + a];
+    c->launches += 1;
+    launch_ktab(c->mkbuf.as<cplx>() + (size_t)i * 9 * c->n, c->d_tw, c->n, s, st);
+    mk.gamma[i] = gamma_rule(c, kpts + 3 * i);
+    mk.thr[i] = pass_threshold(c, kpts + 3 * i);
+  }
+  for (int j = 0; j < ncols; j++) mk.kcol[j] = (unsigned char)kcol[j];
+  return PC_OK;
+}
+static void set_k(pc_ctx* c, const double k[3], cudaStream_t st) {
+  c->cur_gamma = gamma_rule(c, k);
+  if (k[0] == c->cur_k[0] && k[1] == c->cur_k[1] && k[2] == c->cur_k[2]) return;
+  Sym3 s;
+  std::memcpy(s.B, c->B, sizeof(s.B));
+  for (int i = 0; i < 3; i++) s.k[i] = k[i];
+  c->launches += 1;
+  launch_ktab(c->d_ktab, c->d_tw, c->n, s, st);
+  c->cur_thr = pass_threshold(c, k);
   for (int i = 0; i < 3; i++) c->cur_k[i] = k[i];
 }
 
@@ -552,10 +583,11 @@ static ApplyOp paper_op(const pc_ctx* c) { return ApplyOp{c->eps_mode, &c->ec, 0
 
 static int fft_pass(pc_ctx* c, int axis, int dir, int kind, const ColPtrs& in, const MutColPtrs& out,
                     const ColPtrs& xh, int nc, double scale, cudaStream_t st, int z0 = 0, int nz = 0,
-                    int prec = 0, double gamma2 = 0.0) {
+                    int prec = 0, double gamma2 = 0.0, const MultiK* mk = nullptr) {
   PassArgsH a;
   a.tw = c->d_tw;
-  a.ktab = c->d_ktab;
+  a.ktab = (mk && mk->on) ? c->mkbuf.as<cplx>() : c->d_ktab;
+  if (mk && mk->on) a.mk = *mk;
   a.gamma = prec ? 1.0 : c->cur_gamma;
   a.scale = scale;
   a.z0 = z0;
@@ -574,9 +606,10 @@ static ColPtrs to_const(const MutColPtrs& m, int nc) {
   return r;
 }
 
-// Fourier-space apply of nc <= PC_MAXCOLS columns: Y = Op X, ws = nc workspace columns.
+// Fourier-space apply of nc <= PC_MAXCOLS columns: Y = Op X, ws = nc workspace columns.  mk: per-column k
+// (multi-k launch; the symbol passes read each column's own table).
 static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const MutColPtrs& WS, int nc,
-                         cudaStream_t st, const ApplyOp* opp = nullptr) {
+                         cudaStream_t st, const ApplyOp* opp = nullptr, const MultiK* mk = nullptr) {
   const ApplyOp op = opp ? *opp : paper_op(c);
   const int n = c->n;
   const double inv_n3 = 1.0 / ((double)n * n * n);
@@ -595,7 +628,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   for (int j = 0; j < nc; j++) KX.p[j] = c->kxws.as<cplx>() + (size_t)j * c->n3;
   {
     Prof p(c, PC_STAT_FFT_Z_KAH, st, 1, fl + 38.0 * pts, 112.0 * pts);
-    CHK(fft_pass(c, 2, +1, 1, X, Y, KX, nc, inv_n3, st, 0, 0, op.prec));
+    CHK(fft_pass(c, 2, +1, 1, X, Y, KX, nc, inv_n3, st, 0, 0, op.prec, 0.0, mk));
   }
   // z-plane-local media (eps_13 = eps_23 = 0 in CrossDoF; any Diagonal/Trivial medium): the x-passes
   // and the M_eps stencil run fused (x-inverse DFT + M_eps + x-forward DFT in one HBM round trip)
@@ -624,7 +657,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
-      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec));
+      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec, 0.0, mk));
     }
     return PC_OK;
   }
@@ -644,7 +677,7 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
   }
   {
     Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
-    CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec));
+    CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec, 0.0, mk));
   }
   return PC_OK;
 }
@@ -828,6 +861,52 @@ extern "C" int pc_precond(pc_ctx* c, const double k[3], const void* R, void* P, 
       for (int j = 0; j < nc; j++) w.p[j] = c->ws.as<cplx>() + (size_t)j * c->len;
       CHK(precond_eps(c, p, w, nc, st));
     }
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+// Several Bloch vectors in one launch: column j of X is applied with k = kpts[kcol[j]].
+extern "C" int pc_apply_multi(pc_ctx* c, const double* kpts, int nk, const int* kcol, const void* X, void* Y,
+                              int ncols, long long ld, void* stream) {
+  CHK(check_block(c, X, Y, ncols, ld, "pc_apply_multi"));
+  if (!kpts || !kcol) return set_err(PC_EINVAL, "pc_apply_multi: null kpts/kcol");
+  if (X == Y && ncols > 0) return set_err(PC_EINVAL, "pc_apply_multi: X and Y alias");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  const int ch = chunk_cols(c, ncols, 64);
+  CHK(ensure_ws(c, ch));
+  for (int j0 = 0; j0 < ncols; j0 += ch) {
+    const int nc = std::min(ch, ncols - j0);
+    MultiK mk;
+    CHK(build_multik(c, kpts, nk, kcol + j0, nc, mk, st));
+    ColPtrs x;
+    MutColPtrs y, w;
+    block_ptrs(X, ld, j0, nc, x);
+    block_ptrs(Y, ld, j0, nc, y);
+    for (int j = 0; j < nc; j++) w.p[j] = c->ws.as<cplx>() + (size_t)j * c->len;
+    CHK(apply_fourier(c, x, y, w, nc, st, nullptr, &mk));
+  }
+  CU(cudaGetLastError());
+  return PC_OK;
+}
+
+extern "C" int pc_precond_multi(pc_ctx* c, const double* kpts, int nk, const int* kcol, const void* R, void* P,
+                                int ncols, long long ld, void* stream) {
+  CHK(check_block(c, R, P, ncols, ld, "pc_precond_multi"));
+  if (!kpts || !kcol) return set_err(PC_EINVAL, "pc_precond_multi: null kpts/kcol");
+  CU(cudaSetDevice(c->device));
+  cudaStream_t st = (cudaStream_t)stream;
+  for (int j0 = 0; j0 < ncols; j0 += PC_MAXCOLS) {
+    const int nc = std::min(PC_MAXCOLS, ncols - j0);
+    MultiK mk;
+    CHK(build_multik(c, kpts, nk, kcol + j0, nc, mk, st));
+    ColPtrs r;
+    MutColPtrs p;
+    block_ptrs(R, ld, j0, nc, r);
+    block_ptrs(P, ld, j0, nc, p);
+    Prof pf(c, PC_STAT_RESID, st, 1, 60.0 * c->n3 * nc, 96.0 * c->n3 * nc);
+    launch_precond(r, p, nc, c->n, c->mkbuf.as<cplx>(), 0.0, 0.0, st, &mk);
   }
   CU(cudaGetLastError());
   return PC_OK;
@@ -1229,6 +1308,10 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   std::swap(sX, sXn);
   std::swap(sAX, sAXn);
 
+  // P / AP slots: the update's TMA boxes span [first, last] active column, so a column that never got a
+  // P' in this solve (locked from the start) can sit inside a box; C's zero row for it does not cancel a
+  // non-finite leftover of an earlier solve (0 * NaN), so those slots start zeroed (4 b columns)
+  for (int sl : {(int)PA, (int)APA, (int)PB, (int)APB}) CU(cudaMemsetAsync(col(sl, 0), 0, (size_t)b * colb, st));
   std::vector<char> active(b, 1);
   std::vector<double> res(b, 0.0);
   c->hist.clear();

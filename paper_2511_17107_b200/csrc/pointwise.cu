@@ -32,9 +32,15 @@ void launch_ktab(cplx* ktab, const cplx* tw, int n, const Sym3& s, cudaStream_t 
 
 #include "kp.cuh"  // kappa_at, kp_inv
 
-__global__ void precond_kernel(ColPtrs in, MutColPtrs out, int n, const cplx* __restrict__ kt, double gamma,
-                               double thr) {
+__global__ void precond_kernel(ColPtrs in, MutColPtrs out, int n, const cplx* __restrict__ kt0, double gamma,
+                               double thr, MultiK mk) {
   const int col = blockIdx.y;
+  const cplx* kt = kt0;
+  if (mk.on) {  // per-column k (multi-k launch)
+    kt = kt0 + (size_t)mk.kcol[col] * 9 * n;
+    gamma = mk.gamma[mk.kcol[col]];
+    thr = mk.thr[mk.kcol[col]];
+  }
   const cplx* R = in.p[col];
   cplx* P = out.p[col];
   const int n3 = n * n * n;
@@ -51,10 +57,12 @@ __global__ void precond_kernel(ColPtrs in, MutColPtrs out, int n, const cplx* __
 }
 
 void launch_precond(const ColPtrs& in, const MutColPtrs& out, int ncols, int n, const cplx* kt, double gamma,
-                    double thr, cudaStream_t st) {
+                    double thr, cudaStream_t st, const MultiK* mk) {
   long long n3 = (long long)n * n * n;
   int gx = (int)std::min<long long>((n3 + 255) / 256, 148LL * 8);
-  precond_kernel<<<dim3(gx, ncols), 256, 0, st>>>(in, out, n, kt, gamma, thr);
+  MultiK m;
+  if (mk) m = *mk;
+  precond_kernel<<<dim3(gx, ncols), 256, 0, st>>>(in, out, n, kt, gamma, thr, m);
 }
 
 // ------------------------------------------------------------------------------------------

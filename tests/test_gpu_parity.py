@@ -154,6 +154,36 @@ def test_apply_real_space_matches_oracle(api, lat, n, k):
     assert relerr_cols(Y.cpu().numpy(), ref) <= 1e-12
 
 
+@pytest.mark.parametrize("lat,geo,n", [("fcc", "fcc_diamond", 16), ("sc", "sc_curv", 12)])
+def test_apply_and_precond_multi_k_match_oracle(api, lat, geo, n):
+    """several Bloch vectors in one launch (per-column symbol tables, penalties and
+    thresholds), including k = 0 and a k with ||k|| < 1 (gamma = 4 pi^2/||k||^2), against the
+    oracle's apply and K_P^{-1} for each column's own k (<= 1e-12)."""
+    A = synth.lattice(lat)
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks(geo, A, n)
+    kp = np.array([[PI, PI, PI], [0.0, 0.0, 0.0], [0.3, -0.2, 0.5], [1.1, 2.0, -0.4]])
+    kcol = [0, 1, 2, 3, 2, 0, 3]
+    ctx = api.pc_create(A, n, e, masks)
+    x = synth.random_block(n, len(kcol), seed=17)
+    X = to_dev(x)
+    Y = torch.empty_like(X)
+    P = torch.empty_like(X)
+    api.pc_apply_multi(ctx, kp, kcol, X, Y)
+    api.pc_precond_multi(ctx, kp, kcol, X, P)
+    Yh, Ph = Y.cpu().numpy(), P.cpu().numpy()
+    for j, ki in enumerate(kcol):
+        op = O.PenalizedOperator(n, kp[ki], A, e, masks)
+        assert relerr_cols(Yh[j:j + 1], op.apply_fourier(x[j:j + 1])) <= 1e-12
+        ref = O.precond_fourier(n, kp[ki], A, op.gamma, x[j:j + 1])
+        assert relerr_cols(Ph[j:j + 1], ref) <= 1e-12
+    # same result as one-k launches
+    Y1 = torch.empty_like(X)
+    for j, ki in enumerate(kcol):
+        api.pc_apply(ctx, kp[ki], X[j:j + 1], Y1[j:j + 1])
+    assert relerr_cols(Y1.cpu().numpy(), Yh) <= 1e-14
+
+
 def test_apply_gamma_override_and_ld(api):
     """Strided blocks (ld > 3N^3) and the gamma override path."""
     n, A, k = 8, synth.lattice("sc"), (0.2, 0.3, 0.1)
