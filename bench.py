@@ -241,6 +241,17 @@ def oracle_baseline(args, W, steps_kidx, with_c2):
                                       f"tol {args.tol:g}) side by side, k-points / wall (no model)",
                               "iterations": [c["iterations"] for c in c2],
                               "seconds": [round(c["seconds"], 2) for c in c2]}
+    # complete oracle solves of whole paths, measured on the GPU box's host cores (tests/diag/oracle_path_rate.py)
+    meas = {}
+    for wn in ("c2", "c3"):
+        d = load_json(os.path.join(ROOT, "profiles", f"r02_oracle_path_{wn}.json"), None)
+        if d:
+            meas[wn.upper()] = {"kpoints_per_s": d["kpoints_per_s"], "k_points": len(d["k_indices"]),
+                                "workers": d["workers"], "cpu": d["cpu"], "wall_s": d["wall_s"],
+                                "mean_iterations": d["mean_iterations"], "tol": d["tol"],
+                                "source": f"profiles/r02_oracle_path_{wn}.json"}
+    if meas:
+        res["measured_paths"] = meas
     res["paper_timings"] = ("context only: PAPER.md:1260 pseudochiral FCC N=120, 10 bands at (pi,pi,pi): "
                             "GPU 34.15 s (RTX 4090 D, cupy; 0.029 k-points/s), CPU 1506.35 s (numpy, CPU "
                             "model not stated; 0.00066 k-points/s), 55 LOBPCG steps")
