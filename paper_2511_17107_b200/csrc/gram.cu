@@ -192,6 +192,9 @@ __global__ void gram_reduce_kernel(const cplx* partial, int nsplit, int pq, cplx
 #endif
 int grid_cap(int ctas_per_sm) { return std::max(1, 148 * ctas_per_sm); }
 
+static int g_gram_narrow = 1;  // pc_set_option "gram_narrow": the narrow-T block shapes (process-wide)
+void set_gram_narrow(int v) { g_gram_narrow = v ? 1 : 0; }
+
 size_t gram_partial_bytes(int p, int q) { return (size_t)4 * 148 * p * q * sizeof(cplx) + 4096; }
 
 template <int WM, int WN, int WARPS_M, int WARPS_N, int KC, int STAGES, int KS = 1>
@@ -226,7 +229,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
   struct Opt { int bm, bn; };
   const Opt opts[] = {{48, 64}, {48, 48}, {32, 64}, {32, 32}, {40, 40}, {40, 64}, {64, 64}, {80, 64},
                       {80, 96}, {24, 32}, {48, 96}, {40, 24}, {24, 8}, {40, 8}, {24, 16}, {40, 16}};
-  const int nopt = sizeof(opts) / sizeof(opts[0]);
+  const int nopt = g_gram_narrow ? (int)(sizeof(opts) / sizeof(opts[0])) : 12;
   int best = 0;
   double best_cost = 1e300;
   for (int i = 0; i < nopt; i++) {
@@ -257,7 +260,7 @@ void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len
     case 7: PC_GRAM_CASE(5, 2, 2, 4, 16, 3) break;
     case 8: PC_GRAM_CASE(5, 3, 2, 4, 16, 2) break;
     case 9: PC_GRAM_CASE(3, 1, 1, 4, 16, 3) break;
-    case 11: run_gram<5, 1, 1, 3, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;
+    case 11: PC_GRAM_CASE(5, 1, 1, 3, 16, 3) break;
     // narrow T blocks (few active W/P columns in the tail of a solve): one or two 8-column warp tiles,
     // so the row chunks are split over 4 (2) warp groups instead
     case 12: run_gram<3, 1, 1, 1, 16, 3, 4>(S, p, T, q, len, G, partial, st); break;

@@ -99,6 +99,7 @@ size_t gram_partial_bytes(int p, int q);
 void launch_gram_assemble(const cplx* Gp, const double* lam, int b, int c, cplx* G, cudaStream_t st);
 void launch_gram(const ColPtrs& S, int p, const ColPtrs& T, int q, long long len, cplx* G, cplx* partial,
                  cudaStream_t st);
+void set_gram_narrow(int v);  // 1 (default): 8/16-column T block shapes for narrow Grams (process-wide)
 // Block update (r <= 32 output columns, C column-major ld = ldc):
 //   Y1[:, c] = sum_{m in [split, p)} S[:, m] C[m, c]               (if Y1 != nullptr; columns with Y1->p[c] == nullptr skipped)
 //   Y2[:, c] = sum_{m in [0, p)}     S[:, m] C[m, c] (+ add[:, c])

@@ -478,6 +478,7 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "xdev_tol") c->xdev_tol = v;
   else if (k == "update_tmap") c->update_tmap = (int)v;
   else if (k == "jacobi_tol") set_jacobi_tol(v);
+  else if (k == "gram_narrow") set_gram_narrow((int)v);
   else if (k == "start_noise") c->start_noise = v;
   else if (k == "start_precond") c->start_precond = (int)v;
   else return set_err(PC_EINVAL, "pc_set_option: unknown key " + k);
