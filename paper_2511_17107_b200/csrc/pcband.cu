@@ -168,6 +168,9 @@ struct pc_ctx {
   int have_prev = 0, prev_slot = 0, prev_b = 0;
   DevBuf pwbuf;
   DevBuf mkbuf;  // symbol tables of a multi-k launch (PC_MAXK x 9N)
+  int kbatch = 1;                // pc_bands: k-points solved in lock step per batch (solve_batch; 1 = solve_k)
+  double* h_batch = nullptr;     // pinned norms / info of a batch
+  size_t h_batch_n = 0;
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
@@ -422,6 +425,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   c->mkbuf.release();
   auto t3 = now();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
+  if (c->h_batch) cudaFreeHost(c->h_batch);
   auto t4 = now();
   if (c->stream) cudaStreamDestroy(c->stream);
   auto t5 = now();
@@ -460,6 +464,10 @@ extern "C" int pc_set_option(pc_ctx* c, const char* key, double v) {
   else if (k == "drop_tol") c->drop_tol = v;
   else if (k == "kindex_offset") c->kindex_offset = (long long)v;
   else if (k == "verbose") c->verbose = (int)v;
+  else if (k == "kbatch") {
+    if (v < 1 || v > PC_MAXK) return set_err(PC_EINVAL, "kbatch: 1 .. 16");
+    c->kbatch = (int)v;
+  }
   else if (k == "p_restart") c->p_restart = (int)v;
   else if (k == "start") c->start_mode = (int)v;
   else if (k == "warm_start") {
@@ -1107,21 +1115,24 @@ __global__ void normalize_copy_kernel(ColPtrs X, const double* norms, MutColPtrs
 
 // Adds unit transverse plane waves to the b start columns: modes in ascending |kappa|^2 (ties by
 // index), two polarisations u with kappa^T u = 0 (so K_B u = 0) per mode.
-static int plane_wave_start(pc_ctx* c, const MutColPtrs& x0, int b, cudaStream_t st) {
+static int plane_wave_start(pc_ctx* c, const MutColPtrs& x0, int b, cudaStream_t st, const cplx* ktab = nullptr,
+                            double thr = -1.0) {
+  if (!ktab) ktab = c->d_ktab;
+  if (thr < 0.0) thr = c->cur_thr;
   const int G = pw_grid(), n = c->n;
   CHK(c->pwbuf.ensure((size_t)G * PW_T * (sizeof(double) + sizeof(int)) + 64 * sizeof(PwEntry) +
                       9 * n * sizeof(cplx) + 256));
   double* dv = c->pwbuf.as<double>();
   int* di = reinterpret_cast<int*>(dv + G * PW_T);
   PwEntry* de = reinterpret_cast<PwEntry*>(di + G * PW_T + 8);
-  launch_kappa2_topk(c->d_ktab, n, c->cur_thr, dv, di, st);
+  launch_kappa2_topk(ktab, n, thr, dv, di, st);
   double* hv = c->h_pinned + PIN_PWV;
   int* hi = reinterpret_cast<int*>(c->h_pinned + PIN_PWI);
   PwEntry* he = reinterpret_cast<PwEntry*>(c->h_pinned + PIN_PWE);
   std::vector<cplx> kt(9 * n);
   cudaMemcpyAsync(hv, dv, G * PW_T * sizeof(double), cudaMemcpyDeviceToHost, st);
   cudaMemcpyAsync(hi, di, G * PW_T * sizeof(int), cudaMemcpyDeviceToHost, st);
-  cudaMemcpyAsync(kt.data(), c->d_ktab, 9 * n * sizeof(cplx), cudaMemcpyDeviceToHost, st);
+  cudaMemcpyAsync(kt.data(), ktab, 9 * n * sizeof(cplx), cudaMemcpyDeviceToHost, st);
   CU(cudaStreamSynchronize(st));
   std::vector<std::pair<double, int>> cand;
   for (int t = 0; t < G * PW_T; t++)
@@ -1552,6 +1563,440 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
   return conv ? PC_OK : PC_ENOTCONV;
 }
 
+
+// ------------------------------------------------------------------------------------------
+// Batched LOBPCG (k as an extra column dimension).  K k-points run the solve_k algorithm in
+// lock step on one context: per iteration ONE host synchronisation for all residual norms and ONE for all
+// Rayleigh-Ritz ranks (instead of two per k-point), and the operator applies of every k-point's active W
+// columns run as ONE multi-k apply (per-column symbol tables, apply_fourier with MultiK); the Gram,
+// Rayleigh-Ritz and update launches stay per k-point (their blocks are per k).  Same arithmetic as
+// solve_k for each k-point (the multi-k apply computes each column exactly as a one-k apply), so the
+// results equal K separate solves.  Not with warm_start or the eps-weighted preconditioner.
+// ------------------------------------------------------------------------------------------
+struct KSolve {
+  double k[3];
+  int kidx = 0;
+  bool deflate = false;
+  double gamma = 0.0, thr = 0.0;
+  const cplx* kt = nullptr;
+  cplx* base = nullptr;
+  int sX, sAX, sXn, sAXn, sP, sAP, sPn, sAPn;
+  cplx *dG, *dGp, *dC, *dScr;
+  double *dLam, *dNorm, *dPart;
+  int* dInfo;
+  double* hN;
+  int* hInfo;
+  std::vector<char> active, hasW, hasP;
+  std::vector<double> res;
+  std::vector<int> act, actP;
+  bool haveP = false, resid_ready = false, force_full = false, running = true;
+  int it = 0, conv = 0, rank = 0, p = 0, na = 0, nP = 0;
+};
+
+static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev, double tol, int maxit,
+                       unsigned long long seed, double* omega2, double* resid, int* iters, int* status,
+                       cplx* evec_out) {
+  cudaStream_t st = c->stream;
+  const int b = nev + c->guard;
+  const long long len = c->len;
+  const int maxp = 3 * b;
+  if (K * b > PC_MAXCOLS) return set_err(PC_EINVAL, "pc_bands: kbatch x block > 192 columns");
+  const size_t colb = (size_t)len * sizeof(cplx);
+  CHK(c->lob.ensure((size_t)K * 10 * b * colb));
+  CHK(ensure_ws(c, K * b));
+  const size_t nG = (size_t)maxp * 2 * maxp, nC = (size_t)maxp * b, nScr = (size_t)3 * 80 * 80;
+  const int rg = resid_grid(c->n);
+  const size_t per_small = ((2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(3 * b + rg * b * 2) * sizeof(double) +
+                            8 * sizeof(int) + 255) / 256 * 256;
+  CHK(c->small.ensure(per_small * K));
+  CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
+  const size_t hper = 3 * (size_t)b + 8;  // doubles per k: 2b norms, b Ritz values, 8 ints (4 doubles) + pad
+  if (c->h_batch_n < hper * K + (size_t)b) {
+    if (c->h_batch) cudaFreeHost(c->h_batch);
+    c->h_batch = nullptr;
+    c->h_batch_n = 0;
+    if (cudaMallocHost(&c->h_batch, (hper * PC_MAXK + b) * sizeof(double)) != cudaSuccess)
+      return set_err(PC_ENOMEM, "pc_bands: pinned batch buffer");
+    c->h_batch_n = hper * PC_MAXK + b;
+  }
+  const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
+  const bool trim = c->trim_locked != 0;
+  // per-k symbol tables (multi-k buffer), penalties, thresholds
+  MultiK mk;
+  {
+    std::vector<int> kc(K);
+    for (int i = 0; i < K; i++) kc[i] = i;
+    CHK(build_multik(c, kpts, K, kc.data(), K, mk, st));
+  }
+  enum { XA = 0, AXA, XB, AXB, PA, APA, PB, APB, WW, AWW };
+  std::vector<KSolve> ks(K);
+  for (int i = 0; i < K; i++) {
+    KSolve& s = ks[i];
+    for (int a = 0; a < 3; a++) s.k[a] = kpts[3 * i + a];
+    s.kidx = kidx0 + i;
+    s.deflate = (s.k[0] == 0.0 && s.k[1] == 0.0 && s.k[2] == 0.0);
+    s.gamma = mk.gamma[i];
+    s.thr = mk.thr[i];
+    s.kt = c->mkbuf.as<cplx>() + (size_t)i * 9 * c->n;
+    s.base = c->lob.as<cplx>() + (size_t)i * 10 * b * len;
+    s.sX = XA; s.sAX = AXA; s.sXn = XB; s.sAXn = AXB; s.sP = PA; s.sAP = APA; s.sPn = PB; s.sAPn = APB;
+    char* sm = reinterpret_cast<char*>(c->small.p) + per_small * i;
+    s.dG = reinterpret_cast<cplx*>(sm);
+    s.dGp = s.dG + nG;
+    s.dC = s.dGp + nG;
+    s.dScr = s.dC + nC;
+    s.dLam = reinterpret_cast<double*>(s.dScr + nScr);
+    s.dNorm = s.dLam + b;
+    s.dPart = s.dNorm + 2 * b;
+    s.dInfo = reinterpret_cast<int*>(s.dPart + (size_t)rg * b * 2);
+    s.hN = c->h_batch + hper * i;
+    s.hInfo = reinterpret_cast<int*>(s.hN + 3 * b);
+    s.active.assign(b, 1);
+    s.hasW.assign(b, 0);
+    s.hasP.assign(b, 0);
+    s.res.assign(b, 0.0);
+  }
+  auto col = [&](const KSolve& s, int slot, int j) { return s.base + ((size_t)slot * b + j) * len; };
+  std::vector<int> all(b);
+  for (int j = 0; j < b; j++) all[j] = j;
+  auto sync = [&](const char* what) -> int {
+    cudaError_t e = cudaStreamSynchronize(st);
+    if (e == cudaSuccess) e = cudaGetLastError();
+    if (e != cudaSuccess) return set_err(PC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
+    if (c->profile) prof_flush(c);
+    return PC_OK;
+  };
+  auto rr_launch = [&](KSolve& s, int p) {
+    {
+      Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
+      launch_rr(s.dG, p, b, c->drop_tol, s.dC, s.dLam, s.dInfo, s.dScr, st);
+    }
+    cudaMemcpyAsync(s.hInfo, s.dInfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, st);
+  };
+  // one multi-k apply over a list of (k-state, source column, destination column)
+  MutColPtrs wsp;
+  for (int j = 0; j < K * b; j++) wsp.p[j] = c->ws.as<cplx>() + (size_t)j * len;
+  auto apply_batch = [&](const std::vector<std::pair<const cplx*, cplx*>>& cols, const std::vector<int>& kof) -> int {
+    if (cols.empty()) return PC_OK;
+    ColPtrs x;
+    MutColPtrs y;
+    MultiK m = mk;
+    for (size_t t = 0; t < cols.size(); t++) {
+      x.p[t] = cols[t].first;
+      y.p[t] = cols[t].second;
+      m.kcol[t] = (unsigned char)kof[t];
+    }
+    return apply_fourier(c, x, y, wsp, (int)cols.size(), st, nullptr, &m);
+  };
+
+  // ---- start blocks (as solve_k), their applies in one multi-k launch, Rayleigh-Ritz per k
+  for (KSolve& s : ks) {
+    const bool pw = c->start_mode == 1;
+    const bool pre = pw && c->start_precond && c->start_noise > 0.0;
+    const double noise = pw ? c->start_noise / std::sqrt((double)len) * (pre ? 4.0 * M_PI * M_PI : 1.0) : 1.0;
+    Prof pf(c, PC_STAT_OTHER, st, pw ? (pre ? 4 : 3) : 1, 0.0, 16.0 * len * b);
+    MutColPtrs x0;
+    for (int j = 0; j < b; j++) x0.p[j] = col(s, s.sX, j);
+    launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)s.kidx), s.deflate ? (int)c->n3 : 0,
+                 noise, st);
+    if (pre) {
+      ColPtrs xi;
+      for (int j = 0; j < b; j++) xi.p[j] = col(s, s.sX, j);
+      launch_precond(xi, x0, b, c->n, s.kt, s.gamma, s.thr, st);
+    }
+    if (pw) CHK(plane_wave_start(c, x0, b, st, s.kt, s.thr));
+  }
+  {
+    std::vector<std::pair<const cplx*, cplx*>> cols;
+    std::vector<int> kof;
+    for (int i = 0; i < K; i++)
+      for (int j = 0; j < b; j++) {
+        cols.push_back({col(ks[i], ks[i].sX, j), col(ks[i], ks[i].sAX, j)});
+        kof.push_back(i);
+      }
+    CHK(apply_batch(cols, kof));
+  }
+  for (KSolve& s : ks) {
+    ColPtrs S, T;
+    for (int j = 0; j < b; j++) {
+      S.p[j] = col(s, s.sX, j);
+      T.p[j] = col(s, s.sX, j);
+      T.p[b + j] = col(s, s.sAX, j);
+    }
+    {
+      Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * b * 2 * b, 16.0 * len * 2 * b);
+      launch_gram(S, b, T, 2 * b, len, s.dG, c->gpart.as<cplx>(), st);
+    }
+    rr_launch(s, b);
+  }
+  CHK(sync("rayleigh-ritz"));
+  for (KSolve& s : ks) {
+    s.rank = s.hInfo[0];
+    if (s.rank < b) return set_err(PC_ENUMERIC, "pc_bands: start block is rank deficient");
+    Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * b * b, 2 * 16.0 * len * 2 * b);
+    ColPtrs S;
+    MutColPtrs Y;
+    for (int j = 0; j < b; j++) {
+      S.p[j] = col(s, s.sX, j);
+      Y.p[j] = col(s, s.sXn, j);
+    }
+    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, st);
+    for (int j = 0; j < b; j++) {
+      S.p[j] = col(s, s.sAX, j);
+      Y.p[j] = col(s, s.sAXn, j);
+    }
+    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, st);
+    std::swap(s.sX, s.sXn);
+    std::swap(s.sAX, s.sAXn);
+    for (int sl : {(int)PA, (int)APA, (int)PB, (int)APB}) CU(cudaMemsetAsync(col(s, sl, 0), 0, (size_t)b * colb, st));
+  }
+
+  auto resid_cols = [&](KSolve& s, const std::vector<int>& which) {
+    ColPtrs X, AX;
+    MutColPtrs W;
+    for (int j = 0; j < b; j++) {
+      X.p[j] = col(s, s.sX, j);
+      AX.p[j] = col(s, s.sAX, j);
+      W.p[j] = nullptr;
+    }
+    for (int j : which) W.p[j] = col(s, WW, j);
+    Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + (double)which.size()));
+    launch_resid(X, AX, W, s.dLam, b, c->n, s.kt, s.gamma, s.thr, s.deflate ? 1 : 0, s.dPart, s.dNorm, st);
+  };
+
+  for (;;) {
+    // residual norms of every running k-point: one synchronisation
+    for (KSolve& s : ks) {
+      if (!s.running) continue;
+      if (!s.resid_ready) {
+        std::vector<int> w0;
+        for (int j = 0; j < nw; j++) w0.push_back(j);
+        resid_cols(s, w0);
+        for (int j = 0; j < b; j++) s.hasW[j] = j < nw;
+      }
+      cudaMemcpyAsync(s.hN, s.dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
+    }
+    CHK(sync("lobpcg"));
+    int nrun = 0;
+    for (KSolve& s : ks) {
+      if (!s.running) continue;
+      s.conv = 1;
+      double xdev = 0.0;
+      for (int j = 0; j < b; j++) xdev = std::max(xdev, std::fabs(s.hN[2 * j + 1] - 1.0));
+      s.force_full = !(xdev <= c->xdev_tol);
+      for (int j = 0; j < b; j++) s.res[j] = std::sqrt(s.hN[2 * j]) / std::sqrt(s.hN[2 * j + 1]);
+      for (int j = 0; j < b; j++)
+        if (!std::isfinite(s.res[j]))
+          return set_err(PC_ENUMERIC, "pc_bands: non-finite residual at iteration " + std::to_string(s.it));
+      for (int j = 0; j < b; j++) {
+        if (!(s.res[j] > tol)) s.active[j] = 0;
+        else if (!c->sticky_lock) s.active[j] = 1;
+        if (j >= nw) s.active[j] = 0;
+        if (j < nev && !(s.res[j] <= tol)) s.conv = 0;
+      }
+      if (s.force_full && s.it < maxit) {
+        s.conv = 0;
+        bool any = false;
+        for (int j = 0; j < nw; j++) any |= s.active[j] != 0;
+        if (!any)
+          for (int j = 0; j < nw; j++) s.active[j] = 1;
+      }
+      s.act.clear();
+      for (int j = 0; j < b; j++)
+        if (s.active[j]) s.act.push_back(j);
+      if (s.conv || s.it >= maxit || s.act.empty()) {
+        s.running = false;
+        continue;
+      }
+      nrun++;
+      s.na = (int)s.act.size();
+      s.actP.clear();
+      std::vector<int> miss;
+      for (int j : s.act) {
+        if (!trim || s.hasP[j]) s.actP.push_back(j);
+        if (!s.hasW[j]) miss.push_back(j);
+      }
+      if (!miss.empty()) {
+        resid_cols(s, miss);
+        for (int j : miss) s.hasW[j] = 1;
+      }
+      s.nP = (int)s.actP.size();
+    }
+    if (nrun == 0) break;
+    // A W for the active columns of every running k-point: one multi-k apply
+    {
+      std::vector<std::pair<const cplx*, cplx*>> cols;
+      std::vector<int> kof;
+      for (int i = 0; i < K; i++) {
+        if (!ks[i].running) continue;
+        for (int j : ks[i].act) {
+          cols.push_back({col(ks[i], WW, j), col(ks[i], AWW, j)});
+          kof.push_back(i);
+        }
+      }
+      CHK(apply_batch(cols, kof));
+    }
+    // Grams and Rayleigh-Ritz of every running k-point: one synchronisation
+    for (KSolve& s : ks) {
+      if (!s.running) continue;
+      s.p = b + s.na + (s.haveP ? s.nP : 0);
+      const int cw = s.p - b;
+      ColPtrs S, T;
+      for (int j = 0; j < b; j++) S.p[j] = col(s, s.sX, j);
+      for (int t = 0; t < s.na; t++) S.p[b + t] = col(s, WW, s.act[t]);
+      if (s.haveP)
+        for (int t = 0; t < s.nP; t++) S.p[b + s.na + t] = col(s, s.sP, s.actP[t]);
+      const bool full = s.force_full || (c->gram_refresh > 0 && (s.it % c->gram_refresh) == c->gram_refresh - 1);
+      if (full) {
+        for (int t = 0; t < s.p; t++) T.p[t] = S.p[t];
+        for (int j = 0; j < b; j++) T.p[s.p + j] = col(s, s.sAX, j);
+        for (int t = 0; t < s.na; t++) T.p[s.p + b + t] = col(s, AWW, s.act[t]);
+        if (s.haveP)
+          for (int t = 0; t < s.nP; t++) T.p[s.p + b + s.na + t] = col(s, s.sAP, s.actP[t]);
+        Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * s.p * 2 * s.p, 16.0 * len * 2 * s.p);
+        launch_gram(S, s.p, T, 2 * s.p, len, s.dG, c->gpart.as<cplx>(), st);
+      } else {
+        for (int t = 0; t < cw; t++) T.p[t] = S.p[b + t];
+        for (int t = 0; t < s.na; t++) T.p[cw + t] = col(s, AWW, s.act[t]);
+        if (s.haveP)
+          for (int t = 0; t < s.nP; t++) T.p[cw + s.na + t] = col(s, s.sAP, s.actP[t]);
+        Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
+        launch_gram(S, s.p, T, 2 * cw, len, s.dGp, c->gpart.as<cplx>(), st);
+        launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, st);
+      }
+      rr_launch(s, s.p);
+    }
+    CHK(sync("rayleigh-ritz"));
+    for (KSolve& s : ks) {
+      if (!s.running) continue;
+      s.rank = s.hInfo[0];
+      // rank deficient with P: restart this k-point without the P block (rare; its own synchronisation)
+      while (!(s.rank >= s.p || (s.rank >= b && !c->p_restart) || (s.rank >= b && !s.haveP))) {
+        if (!s.haveP)
+          return set_err(PC_ENUMERIC, "pc_bands: Rayleigh-Ritz basis collapsed (rank " + std::to_string(s.rank) +
+                                          " < " + std::to_string(b) + ")");
+        s.haveP = false;
+        s.p = b + s.na;
+        const int cw = s.na;
+        ColPtrs S, T;
+        for (int j = 0; j < b; j++) S.p[j] = col(s, s.sX, j);
+        for (int t = 0; t < s.na; t++) {
+          S.p[b + t] = col(s, WW, s.act[t]);
+          T.p[t] = S.p[b + t];
+          T.p[cw + t] = col(s, AWW, s.act[t]);
+        }
+        {
+          Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
+          launch_gram(S, s.p, T, 2 * cw, len, s.dGp, c->gpart.as<cplx>(), st);
+          launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, st);
+        }
+        rr_launch(s, s.p);
+        CHK(sync("rayleigh-ritz"));
+        s.rank = s.hInfo[0];
+      }
+    }
+    // updates (+ next residual, W = K_P^{-1} R) per k-point
+    for (KSolve& s : ks) {
+      if (!s.running) continue;
+      std::vector<char> wr(b, 0);
+      for (int j = 0; j < nw; j++) wr[j] = 1;
+      if (trim) {
+        for (int j = 0; j < b; j++) wr[j] = 0;
+        for (int j : s.act) wr[j] = 1;
+      }
+      MutColPtrs Y1, Y2, Y1a, Y2a, W;
+      for (int j = 0; j < b; j++) {
+        Y1.p[j] = wr[j] ? col(s, s.sPn, j) : nullptr;
+        Y2.p[j] = col(s, s.sXn, j);
+        Y1a.p[j] = wr[j] ? col(s, s.sAPn, j) : nullptr;
+        Y2a.p[j] = col(s, s.sAXn, j);
+        W.p[j] = wr[j] ? col(s, WW, j) : nullptr;
+        s.hasP[j] = wr[j];
+        s.hasW[j] = wr[j];
+      }
+      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * s.p * b + 84.0 * c->n3 * b,
+              16.0 * len * (2 * s.p + 2 * (b + nw) + nw));
+      int g = -1;
+      if (c->update_tmap && update_tmap_supported(c->n, b)) {
+        UtBlocks blk;
+        memset(&blk, 0, sizeof(blk));
+        blk.ld = len;
+        const int slotS[3] = {s.sX, WW, s.sP}, slotA[3] = {s.sAX, AWW, s.sAP};
+        const std::vector<int>* lists[3] = {&all, &s.act, &s.actP};
+        const int rowoff[3] = {0, b, b + s.na};
+        for (int kb = 0; kb < 3; kb++) {
+          const std::vector<int>& L = *lists[kb];
+          if (L.empty() || (kb == 2 && !s.haveP)) continue;
+          blk.s[kb] = col(s, slotS[kb], 0);
+          blk.as[kb] = col(s, slotA[kb], 0);
+          blk.slot_cols[kb] = b;
+          blk.c0[kb] = L.front();
+          blk.nc[kb] = L.back() - L.front() + 1;
+          for (int j = 0; j < 32; j++) blk.crow[kb][j] = -1;
+          for (size_t t = 0; t < L.size(); t++) blk.crow[kb][L[t] - L.front()] = (signed char)(rowoff[kb] + t);
+        }
+        g = launch_update_tmap(blk, s.dC, s.p, b, Y1, Y2, Y1a, Y2a, W, s.dLam, c->n, s.kt, s.gamma, s.thr,
+                               s.deflate ? 1 : 0, s.dPart, rg, st);
+      }
+      if (g < 0) {
+        ColPtrs S, AS;
+        for (int j = 0; j < b; j++) {
+          S.p[j] = col(s, s.sX, j);
+          AS.p[j] = col(s, s.sAX, j);
+        }
+        for (int t = 0; t < s.na; t++) {
+          S.p[b + t] = col(s, WW, s.act[t]);
+          AS.p[b + t] = col(s, AWW, s.act[t]);
+        }
+        if (s.haveP)
+          for (int t = 0; t < s.nP; t++) {
+            S.p[b + s.na + t] = col(s, s.sP, s.actP[t]);
+            AS.p[b + s.na + t] = col(s, s.sAP, s.actP[t]);
+          }
+        g = launch_update_all(S, AS, s.p, s.dC, s.p, b, b, Y1, Y2, Y1a, Y2a, W, s.dLam, c->n, s.kt, s.gamma, s.thr,
+                              s.deflate ? 1 : 0, s.dPart, rg, st);
+      }
+      launch_reduce_partial(s.dPart, g, b, s.dNorm, st);
+      s.resid_ready = true;
+      std::swap(s.sX, s.sXn);
+      std::swap(s.sAX, s.sAXn);
+      std::swap(s.sP, s.sPn);
+      std::swap(s.sAP, s.sAPn);
+      s.haveP = true;
+      s.it++;
+    }
+  }
+  // outputs
+  int rc = PC_OK;
+  for (int i = 0; i < K; i++) {
+    KSolve& s = ks[i];
+    cudaMemcpyAsync(s.hN + 2 * b, s.dLam, b * sizeof(double), cudaMemcpyDeviceToHost, st);
+    if (evec_out) {
+      ColPtrs X;
+      MutColPtrs Y;
+      for (int j = 0; j < nev; j++) {
+        X.p[j] = col(s, s.sX, j);
+        Y.p[j] = evec_out + ((size_t)i * nev + j) * len;
+      }
+      c->launches += 1;
+      normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, st>>>(X, s.dNorm, Y, len);
+    }
+  }
+  CHK(sync("lobpcg"));
+  for (int i = 0; i < K; i++) {
+    KSolve& s = ks[i];
+    for (int j = 0; j < nev; j++) {
+      omega2[(size_t)i * nev + j] = s.hN[2 * b + j];
+      if (resid) resid[(size_t)i * nev + j] = s.res[j];
+    }
+    if (iters) iters[i] = s.it;
+    if (status) status[i] = s.conv ? 0 : 1;
+    if (!s.conv) rc = PC_ENOTCONV;
+  }
+  c->have_prev = 0;
+  return rc;
+}
+
 extern "C" int pc_bands(pc_ctx* c, const double* kpts, int nk, int nev, double tol, int maxit,
                         unsigned long long seed, double* omega2, double* resid, int* iters, int* status, void* evecs) {
   if (!c || (!kpts && nk > 0) || (!omega2 && nk > 0)) return set_err(PC_EINVAL, "pc_bands: null argument");
@@ -1560,6 +2005,19 @@ extern "C" int pc_bands(pc_ctx* c, const double* kpts, int nk, int nev, double t
   if (3 * b > 80) return set_err(PC_EINVAL, "pc_bands: nev + guard must be <= 26");
   CU(cudaSetDevice(c->device));
   int rc_all = PC_OK;
+  if (c->kbatch > 1 && !c->warm_start && c->precond == 0) {
+    // k-points in lock step, c->kbatch at a time
+    for (int i0 = 0; i0 < nk; i0 += c->kbatch) {
+      const int K = std::min(c->kbatch, nk - i0);
+      int rc = solve_batch(c, kpts + 3 * i0, K, (int)(c->kindex_offset + i0), nev, tol, maxit, seed,
+                           omega2 + (size_t)i0 * nev, resid ? resid + (size_t)i0 * nev : nullptr,
+                           iters ? iters + i0 : nullptr, status ? status + i0 : nullptr,
+                           evecs ? reinterpret_cast<cplx*>(evecs) + (size_t)i0 * nev * c->len : nullptr);
+      if (rc < 0) return rc;
+      if (rc == PC_ENOTCONV) rc_all = PC_ENOTCONV;
+    }
+    return rc_all;
+  }
   for (int i = 0; i < nk; i++) {
     cplx* ev = evecs ? reinterpret_cast<cplx*>(evecs) + (size_t)i * nev * c->len : nullptr;
     int st_i = 0, it_i = 0;
