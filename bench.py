@@ -324,6 +324,8 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--guard", type=int, default=None, help="LOBPCG guard columns (block = nev + guard)")
     ap.add_argument("--streams", type=int, default=2, help="concurrent k-point solves per GPU (contexts)")
+    ap.add_argument("--kbatch", type=int, default=1,
+                    help="k-points solved in lock step per pc_bands call (option kbatch; helps at n <= 64)")
     ap.add_argument("--w-guard", type=int, default=None, help="guard columns that get search directions")
     ap.add_argument("--warm-start", action="store_true",
                     help="path continuation: contiguous k stretches per context, each k started from the "
@@ -403,7 +405,7 @@ def main():
             return bands.solve_warm(ctxs, kp, idx_list, W.nev, args.tol, args.maxit, 0)
         ks = sorted({kidx(s_, r) for r in range(world) for s_ in svals})
         res = bands.band_structure(ctxs, kp, nev=W.nev, tol=args.tol, maxit=args.maxit, seed=0,
-                                   device=cdev, ks=ks)
+                                   device=cdev, ks=ks, kbatch=args.kbatch)
         sel = np.array(idx_list, dtype=np.int64)
         return res["omega2"][sel], res["resid"][sel], res["iters"][sel], res["status"][sel]
 
@@ -601,7 +603,8 @@ def main():
                     api.pc_set_option(c_, "w_guard", args.w_guard)
                 api.pc_set_option(c_, "precond", 1 if args.precond == "eps" else 0)
             res = bands.band_structure(ce, kp, nev=W.nev, tol=args.tol, maxit=args.maxit, seed=0, device=cdev,
-                                       ks=sorted({kidx(s_, r) for r in range(world) for s_ in svals}))
+                                       ks=sorted({kidx(s_, r) for r in range(world) for s_ in svals}),
+                                       kbatch=args.kbatch)
             sel = np.array(idx_list, dtype=np.int64)
             out = (res["omega2"][sel], res["resid"][sel], res["iters"][sel], res["status"][sel])
             for c_ in ce:

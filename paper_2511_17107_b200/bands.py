@@ -63,6 +63,18 @@ class KQueue:
         return self.order[t] if t < len(self.order) else None
 
 
+class ChunkQueue(KQueue):
+    """A KQueue whose items are chunks (lists) of k indices."""
+
+    def __init__(self, chunks, store=None, key: str = "pcband/kq"):
+        super().__init__(range(len(chunks)), store, key)
+        self.chunks = [list(ch) for ch in chunks]
+
+    def next(self):
+        t = super().next()
+        return None if t is None else self.chunks[t]
+
+
 def longest_first(idx, cost=None) -> list:
     """Hand-out order: descending estimated cost (ties and cost=None: the given order)."""
     idx = [int(g) for g in idx]
@@ -75,24 +87,42 @@ def longest_first(idx, cost=None) -> list:
 _JOBS = [0]
 
 
-def job_queue(idx, cost=None, group=None) -> KQueue:
+def job_queue(idx, cost=None, group=None, kbatch: int = 1) -> KQueue:
     """A KQueue over idx for this job: across ranks through the default process group's store
     (world > 1), else a local counter.  Collective in the sense that every rank must call it the
     same number of times (the counter key is numbered per call)."""
     import torch.distributed as dist
     order = longest_first(idx, cost)
     _JOBS[0] += 1
+    store, key = None, "pcband/kq"
     if dist.is_initialized() and dist.get_world_size(group) > 1:
         from torch.distributed import distributed_c10d as c10d
-        store = c10d._get_default_store()
-        return KQueue(order, store, key=f"pcband/kq/{_JOBS[0]}")
-    return KQueue(order)
+        store, key = c10d._get_default_store(), f"pcband/kq/{_JOBS[0]}"
+    if kbatch > 1:  # chunks of consecutive path points (lock-step batches), in index order
+        srt = sorted(int(g) for g in idx)
+        return ChunkQueue([srt[i:i + kbatch] for i in range(0, len(srt), kbatch)], store, key)
+    return KQueue(order, store, key)
 
 
-def solve_queue(ctxs, kpts: np.ndarray, queue: KQueue, nev: int, tol: float, maxit: int, seed: int):
+def runs(ks):
+    """Split a list of k indices into runs of consecutive integers (pc_bands keys the start block of its
+    i-th k-point by kindex_offset + i)."""
+    out = []
+    for g in ks:
+        if out and g == out[-1][-1] + 1:
+            out[-1].append(g)
+        else:
+            out.append([g])
+    return out
+
+
+def solve_queue(ctxs, kpts: np.ndarray, queue: KQueue, nev: int, tol: float, maxit: int, seed: int,
+                kbatch: int = 1):
     """Solve k-points drawn from `queue` with the contexts ctxs (one host thread per context; ctypes
-    releases the GIL during pc_bands) until the queue is empty.  Returns (idx, omega2, Res, iters,
-    status) for the k-points this process solved, in the order they were drawn."""
+    releases the GIL during pc_bands) until the queue is empty.  kbatch > 1: each draw hands out a chunk of
+    kbatch k-points (queue items are chunk numbers of chunked(ks, kbatch)), solved in lock step by one
+    pc_bands call per run of consecutive indices (option "kbatch").  Returns (idx, omega2, Res,
+    iters, status) for the k-points this process solved, in the order they were drawn."""
     from . import api
     if not isinstance(ctxs, (list, tuple)):
         ctxs = [ctxs]
@@ -102,14 +132,18 @@ def solve_queue(ctxs, kpts: np.ndarray, queue: KQueue, nev: int, tol: float, max
 
     def worker(ctx):
         try:
+            if kbatch > 1:
+                api.pc_set_option(ctx, "kbatch", kbatch)
             while True:
-                g = queue.next()
-                if g is None:
+                item = queue.next()
+                if item is None:
                     return
-                api.pc_set_option(ctx, "kindex_offset", g)
-                r = api.pc_bands(ctx, kpts[g:g + 1], nev=nev, tol=tol, maxit=maxit, seed=seed)
-                with lock:
-                    rows.append((g, r["omega2"][0], r["resid"][0], int(r["iters"][0]), int(r["status"][0])))
+                for run in runs(item if isinstance(item, list) else [item]):
+                    api.pc_set_option(ctx, "kindex_offset", run[0])
+                    r = api.pc_bands(ctx, kpts[run], nev=nev, tol=tol, maxit=maxit, seed=seed)
+                    with lock:
+                        for t, g in enumerate(run):
+                            rows.append((g, r["omega2"][t], r["resid"][t], int(r["iters"][t]), int(r["status"][t])))
         except Exception as ex:  # pragma: no cover - surfaced below
             errors.append(ex)
 
@@ -236,16 +270,19 @@ def gather(om, rs, it, stt, idx, nk, group=None, device=None, cap=None, ks=None)
 
 
 def band_structure(ctxs, kpts, nev=10, tol=1e-5, maxit=500, seed=0, group=None, device=None,
-                   solver: Callable | None = None, cost=None, ks=None):
+                   solver: Callable | None = None, cost=None, ks=None, kbatch: int = 1):
     """Full band structure through the public API: the k-points (all of kpts, or the global indices
     ks) are drawn from a dynamic queue shared by every rank (longest-first by `cost` if given), solved
     by this rank's contexts ctxs (one or a list: concurrent solves on one GPU), and gathered with one
     all-gather.  Every rank returns the full result in k order.  `solver(ctxs, kpts, queue, nev, tol,
-    maxit, seed)` replaces solve_queue in host-logic tests (a CPU stub under gloo)."""
+    maxit, seed)` replaces solve_queue in host-logic tests (a CPU stub under gloo).  kbatch > 1: chunks of
+    kbatch consecutive k-points are drawn and solved in lock step (option "kbatch"; n <= 64)."""
     kpts = np.asarray(kpts, dtype=np.float64).reshape(-1, 3)
     nk = kpts.shape[0]
     ks = list(range(nk)) if ks is None else [int(g) for g in ks]
-    q = job_queue(ks, cost, group)
-    fn = solver or solve_queue
-    idx, om, rs, it, stt = fn(ctxs, kpts, q, nev, tol, maxit, seed)
+    q = job_queue(ks, cost, group, kbatch)
+    if solver is None:
+        idx, om, rs, it, stt = solve_queue(ctxs, kpts, q, nev, tol, maxit, seed, kbatch)
+    else:
+        idx, om, rs, it, stt = solver(ctxs, kpts, q, nev, tol, maxit, seed)
     return gather(om, rs, it, stt, idx, nk, group=group, device=device, cap=len(ks), ks=ks)

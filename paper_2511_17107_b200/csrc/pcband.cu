@@ -171,6 +171,8 @@ struct pc_ctx {
   int kbatch = 1;                // pc_bands: k-points solved in lock step per batch (solve_batch; 1 = solve_k)
   double* h_batch = nullptr;     // pinned norms / info of a batch
   size_t h_batch_n = 0;
+  std::vector<cudaStream_t> bst; // per-k streams of a batch (the per-k Gram / Rayleigh-Ritz / update launches)
+  std::vector<cudaEvent_t> bev;
   std::vector<double> hist;  // Res_j per iteration of the last solved k-point (row-major, hist_b per row)
   int hist_b = 0;
   // LOBPCG storage
@@ -426,6 +428,8 @@ extern "C" void pc_destroy(pc_ctx* c) {
   auto t3 = now();
   if (c->h_pinned) cudaFreeHost(c->h_pinned);
   if (c->h_batch) cudaFreeHost(c->h_batch);
+  for (auto s_ : c->bst) cudaStreamDestroy(s_);
+  for (auto e_ : c->bev) cudaEventDestroy(e_);
   auto t4 = now();
   if (c->stream) cudaStreamDestroy(c->stream);
   auto t5 = now();
@@ -663,6 +667,28 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
         Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
         CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
       }
+    }
+    {
+      Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
+      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec, 0.0, mk));
+    }
+    return PC_OK;
+  }
+  if (c->fuse_xex) {
+    // general CrossDoF medium (S_13 / S_23 couple z-neighbours): y-inverse, then x-inverse + M_eps +
+    // x-forward in one z-walking pass (xexg), y-forward, z + K_A + gamma K_B: 5 passes
+    {
+      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+      CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
+    }
+    {
+      Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 150.0 * pts, 109.0 * pts);
+      cudaError_t e = launch_xexg(n, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, 1.0, st);
+      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xexg pass: ") + cudaGetErrorString(e));
+    }
+    {
+      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
+      CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
     }
     {
       Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
@@ -1574,6 +1600,7 @@ static int solve_k(pc_ctx* c, const double k[3], int kidx, int nev, double tol, 
 // results equal K separate solves.  Not with warm_start or the eps-weighted preconditioner.
 // ------------------------------------------------------------------------------------------
 struct KSolve {
+  cudaStream_t stm = nullptr;  // this k-point's stream
   double k[3];
   int kidx = 0;
   bool deflate = false;
@@ -1609,7 +1636,8 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
   const size_t per_small = ((2 * nG + nC + nScr) * sizeof(cplx) + (size_t)(3 * b + rg * b * 2) * sizeof(double) +
                             8 * sizeof(int) + 255) / 256 * 256;
   CHK(c->small.ensure(per_small * K));
-  CHK(c->gpart.ensure(gram_partial_bytes(maxp, 2 * maxp)));
+  const size_t gpb = (gram_partial_bytes(maxp, 2 * maxp) + 255) / 256 * 256;
+  CHK(c->gpart.ensure(gpb * K));  // one Gram split-K partial buffer per k-point (per-k streams run concurrently)
   const size_t hper = 3 * (size_t)b + 8;  // doubles per k: 2b norms, b Ritz values, 8 ints (4 doubles) + pad
   if (c->h_batch_n < hper * K + (size_t)b) {
     if (c->h_batch) cudaFreeHost(c->h_batch);
@@ -1621,6 +1649,34 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
   }
   const int nw = (c->w_guard >= 0) ? std::min(b, nev + c->w_guard) : b;
   const bool trim = c->trim_locked != 0;
+  // per-k streams: k-point i's own launches run on bst[i], so those of different k-points overlap (at
+  // n <= 64 one k-point's kernels fill a fraction of the GPU); the multi-k applies run on the context
+  // stream between an event join and an event fork
+  while ((int)c->bst.size() < K) {
+    cudaStream_t s_;
+    cudaEvent_t e_;
+    if (cudaStreamCreateWithFlags(&s_, cudaStreamNonBlocking) != cudaSuccess) return set_err(PC_ECUDA, "batch streams");
+    cudaEventCreateWithFlags(&e_, cudaEventDisableTiming);
+    c->bst.push_back(s_);
+    c->bev.push_back(e_);
+  }
+  cudaEvent_t ev_main = nullptr;
+  if (c->bev.size() < (size_t)K + 1) {
+    cudaEvent_t e_;
+    cudaEventCreateWithFlags(&e_, cudaEventDisableTiming);
+    c->bev.push_back(e_);
+  }
+  ev_main = c->bev[K];
+  auto join = [&]() {  // context stream waits for every per-k stream
+    for (int i = 0; i < K; i++) {
+      cudaEventRecord(c->bev[i], c->bst[i]);
+      cudaStreamWaitEvent(st, c->bev[i], 0);
+    }
+  };
+  auto fork = [&]() {  // every per-k stream waits for the context stream
+    cudaEventRecord(ev_main, st);
+    for (int i = 0; i < K; i++) cudaStreamWaitEvent(c->bst[i], ev_main, 0);
+  };
   // per-k symbol tables (multi-k buffer), penalties, thresholds
   MultiK mk;
   {
@@ -1628,6 +1684,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
     for (int i = 0; i < K; i++) kc[i] = i;
     CHK(build_multik(c, kpts, K, kc.data(), K, mk, st));
   }
+  fork();
   enum { XA = 0, AXA, XB, AXB, PA, APA, PB, APB, WW, AWW };
   std::vector<KSolve> ks(K);
   for (int i = 0; i < K; i++) {
@@ -1638,6 +1695,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
     s.gamma = mk.gamma[i];
     s.thr = mk.thr[i];
     s.kt = c->mkbuf.as<cplx>() + (size_t)i * 9 * c->n;
+    s.stm = c->bst[i];
     s.base = c->lob.as<cplx>() + (size_t)i * 10 * b * len;
     s.sX = XA; s.sAX = AXA; s.sXn = XB; s.sAXn = AXB; s.sP = PA; s.sAP = APA; s.sPn = PB; s.sAPn = APB;
     char* sm = reinterpret_cast<char*>(c->small.p) + per_small * i;
@@ -1657,9 +1715,13 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
     s.res.assign(b, 0.0);
   }
   auto col = [&](const KSolve& s, int slot, int j) { return s.base + ((size_t)slot * b + j) * len; };
+  auto gpart_of = [&](const KSolve& s) {
+    return reinterpret_cast<cplx*>(reinterpret_cast<char*>(c->gpart.p) + gpb * (size_t)(&s - ks.data()));
+  };
   std::vector<int> all(b);
   for (int j = 0; j < b; j++) all[j] = j;
   auto sync = [&](const char* what) -> int {
+    join();
     cudaError_t e = cudaStreamSynchronize(st);
     if (e == cudaSuccess) e = cudaGetLastError();
     if (e != cudaSuccess) return set_err(PC_ECUDA, std::string(what) + ": " + cudaGetErrorString(e));
@@ -1668,10 +1730,10 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
   };
   auto rr_launch = [&](KSolve& s, int p) {
     {
-      Prof pf(c, PC_STAT_RR, st, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
-      launch_rr(s.dG, p, b, c->drop_tol, s.dC, s.dLam, s.dInfo, s.dScr, st);
+      Prof pf(c, PC_STAT_RR, s.stm, 1, 16.0 * 8.0 * 8.0 * (double)p * p * p, 0.0);
+      launch_rr(s.dG, p, b, c->drop_tol, s.dC, s.dLam, s.dInfo, s.dScr, s.stm);
     }
-    cudaMemcpyAsync(s.hInfo, s.dInfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(s.hInfo, s.dInfo, 8 * sizeof(int), cudaMemcpyDeviceToHost, s.stm);
   };
   // one multi-k apply over a list of (k-state, source column, destination column)
   MutColPtrs wsp;
@@ -1686,7 +1748,10 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
       y.p[t] = cols[t].second;
       m.kcol[t] = (unsigned char)kof[t];
     }
-    return apply_fourier(c, x, y, wsp, (int)cols.size(), st, nullptr, &m);
+    join();
+    const int rc = apply_fourier(c, x, y, wsp, (int)cols.size(), st, nullptr, &m);
+    fork();
+    return rc;
   };
 
   // ---- start blocks (as solve_k), their applies in one multi-k launch, Rayleigh-Ritz per k
@@ -1694,17 +1759,20 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
     const bool pw = c->start_mode == 1;
     const bool pre = pw && c->start_precond && c->start_noise > 0.0;
     const double noise = pw ? c->start_noise / std::sqrt((double)len) * (pre ? 4.0 * M_PI * M_PI : 1.0) : 1.0;
-    Prof pf(c, PC_STAT_OTHER, st, pw ? (pre ? 4 : 3) : 1, 0.0, 16.0 * len * b);
+    Prof pf(c, PC_STAT_OTHER, s.stm, pw ? (pre ? 4 : 3) : 1, 0.0, 16.0 * len * b);
     MutColPtrs x0;
     for (int j = 0; j < b; j++) x0.p[j] = col(s, s.sX, j);
     launch_randn(x0, b, len, mix64(seed + 0x100000001ull * (unsigned long long)s.kidx), s.deflate ? (int)c->n3 : 0,
-                 noise, st);
+                 noise, s.stm);
     if (pre) {
       ColPtrs xi;
       for (int j = 0; j < b; j++) xi.p[j] = col(s, s.sX, j);
-      launch_precond(xi, x0, b, c->n, s.kt, s.gamma, s.thr, st);
+      launch_precond(xi, x0, b, c->n, s.kt, s.gamma, s.thr, s.stm);
     }
-    if (pw) CHK(plane_wave_start(c, x0, b, st, s.kt, s.thr));
+    if (pw) {
+      CHK(plane_wave_start(c, x0, b, s.stm, s.kt, s.thr));
+      CU(cudaStreamSynchronize(s.stm));  // the context's plane-wave scratch is reused by the next k-point
+    }
   }
   {
     std::vector<std::pair<const cplx*, cplx*>> cols;
@@ -1724,8 +1792,8 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
       T.p[b + j] = col(s, s.sAX, j);
     }
     {
-      Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * b * 2 * b, 16.0 * len * 2 * b);
-      launch_gram(S, b, T, 2 * b, len, s.dG, c->gpart.as<cplx>(), st);
+      Prof pf(c, PC_STAT_GRAM, s.stm, 2, 8.0 * len * b * 2 * b, 16.0 * len * 2 * b);
+      launch_gram(S, b, T, 2 * b, len, s.dG, gpart_of(s), s.stm);
     }
     rr_launch(s, b);
   }
@@ -1733,22 +1801,23 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
   for (KSolve& s : ks) {
     s.rank = s.hInfo[0];
     if (s.rank < b) return set_err(PC_ENUMERIC, "pc_bands: start block is rank deficient");
-    Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * b * b, 2 * 16.0 * len * 2 * b);
+    Prof pf(c, PC_STAT_UPDATE, s.stm, 2, 2 * 8.0 * len * b * b, 2 * 16.0 * len * 2 * b);
     ColPtrs S;
     MutColPtrs Y;
     for (int j = 0; j < b; j++) {
       S.p[j] = col(s, s.sX, j);
       Y.p[j] = col(s, s.sXn, j);
     }
-    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, st);
+    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, s.stm);
     for (int j = 0; j < b; j++) {
       S.p[j] = col(s, s.sAX, j);
       Y.p[j] = col(s, s.sAXn, j);
     }
-    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, st);
+    launch_update(S, b, s.dC, b, b, b, nullptr, Y, nullptr, len, s.stm);
     std::swap(s.sX, s.sXn);
     std::swap(s.sAX, s.sAXn);
-    for (int sl : {(int)PA, (int)APA, (int)PB, (int)APB}) CU(cudaMemsetAsync(col(s, sl, 0), 0, (size_t)b * colb, st));
+    for (int sl : {(int)PA, (int)APA, (int)PB, (int)APB})
+      CU(cudaMemsetAsync(col(s, sl, 0), 0, (size_t)b * colb, s.stm));
   }
 
   auto resid_cols = [&](KSolve& s, const std::vector<int>& which) {
@@ -1760,8 +1829,8 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
       W.p[j] = nullptr;
     }
     for (int j : which) W.p[j] = col(s, WW, j);
-    Prof pf(c, PC_STAT_RESID, st, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + (double)which.size()));
-    launch_resid(X, AX, W, s.dLam, b, c->n, s.kt, s.gamma, s.thr, s.deflate ? 1 : 0, s.dPart, s.dNorm, st);
+    Prof pf(c, PC_STAT_RESID, s.stm, 2, 84.0 * c->n3 * b, 16.0 * len * (2 * b + (double)which.size()));
+    launch_resid(X, AX, W, s.dLam, b, c->n, s.kt, s.gamma, s.thr, s.deflate ? 1 : 0, s.dPart, s.dNorm, s.stm);
   };
 
   for (;;) {
@@ -1774,7 +1843,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
         resid_cols(s, w0);
         for (int j = 0; j < b; j++) s.hasW[j] = j < nw;
       }
-      cudaMemcpyAsync(s.hN, s.dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, st);
+      cudaMemcpyAsync(s.hN, s.dNorm, 2 * b * sizeof(double), cudaMemcpyDeviceToHost, s.stm);
     }
     CHK(sync("lobpcg"));
     int nrun = 0;
@@ -1853,16 +1922,16 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
         for (int t = 0; t < s.na; t++) T.p[s.p + b + t] = col(s, AWW, s.act[t]);
         if (s.haveP)
           for (int t = 0; t < s.nP; t++) T.p[s.p + b + s.na + t] = col(s, s.sAP, s.actP[t]);
-        Prof pf(c, PC_STAT_GRAM, st, 2, 8.0 * len * s.p * 2 * s.p, 16.0 * len * 2 * s.p);
-        launch_gram(S, s.p, T, 2 * s.p, len, s.dG, c->gpart.as<cplx>(), st);
+        Prof pf(c, PC_STAT_GRAM, s.stm, 2, 8.0 * len * s.p * 2 * s.p, 16.0 * len * 2 * s.p);
+        launch_gram(S, s.p, T, 2 * s.p, len, s.dG, gpart_of(s), s.stm);
       } else {
         for (int t = 0; t < cw; t++) T.p[t] = S.p[b + t];
         for (int t = 0; t < s.na; t++) T.p[cw + t] = col(s, AWW, s.act[t]);
         if (s.haveP)
           for (int t = 0; t < s.nP; t++) T.p[cw + s.na + t] = col(s, s.sAP, s.actP[t]);
-        Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
-        launch_gram(S, s.p, T, 2 * cw, len, s.dGp, c->gpart.as<cplx>(), st);
-        launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, st);
+        Prof pf(c, PC_STAT_GRAM, s.stm, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
+        launch_gram(S, s.p, T, 2 * cw, len, s.dGp, gpart_of(s), s.stm);
+        launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, s.stm);
       }
       rr_launch(s, s.p);
     }
@@ -1886,9 +1955,9 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
           T.p[cw + t] = col(s, AWW, s.act[t]);
         }
         {
-          Prof pf(c, PC_STAT_GRAM, st, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
-          launch_gram(S, s.p, T, 2 * cw, len, s.dGp, c->gpart.as<cplx>(), st);
-          launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, st);
+          Prof pf(c, PC_STAT_GRAM, s.stm, 3, 8.0 * len * s.p * 2 * cw, 16.0 * len * (s.p + cw));
+          launch_gram(S, s.p, T, 2 * cw, len, s.dGp, gpart_of(s), s.stm);
+          launch_gram_assemble(s.dGp, s.dLam, b, cw, s.dG, s.stm);
         }
         rr_launch(s, s.p);
         CHK(sync("rayleigh-ritz"));
@@ -1914,7 +1983,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
         s.hasP[j] = wr[j];
         s.hasW[j] = wr[j];
       }
-      Prof pf(c, PC_STAT_UPDATE, st, 2, 2 * 8.0 * len * s.p * b + 84.0 * c->n3 * b,
+      Prof pf(c, PC_STAT_UPDATE, s.stm, 2, 2 * 8.0 * len * s.p * b + 84.0 * c->n3 * b,
               16.0 * len * (2 * s.p + 2 * (b + nw) + nw));
       int g = -1;
       if (c->update_tmap && update_tmap_supported(c->n, b)) {
@@ -1936,7 +2005,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
           for (size_t t = 0; t < L.size(); t++) blk.crow[kb][L[t] - L.front()] = (signed char)(rowoff[kb] + t);
         }
         g = launch_update_tmap(blk, s.dC, s.p, b, Y1, Y2, Y1a, Y2a, W, s.dLam, c->n, s.kt, s.gamma, s.thr,
-                               s.deflate ? 1 : 0, s.dPart, rg, st);
+                               s.deflate ? 1 : 0, s.dPart, rg, s.stm);
       }
       if (g < 0) {
         ColPtrs S, AS;
@@ -1954,9 +2023,9 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
             AS.p[b + s.na + t] = col(s, s.sAP, s.actP[t]);
           }
         g = launch_update_all(S, AS, s.p, s.dC, s.p, b, b, Y1, Y2, Y1a, Y2a, W, s.dLam, c->n, s.kt, s.gamma, s.thr,
-                              s.deflate ? 1 : 0, s.dPart, rg, st);
+                              s.deflate ? 1 : 0, s.dPart, rg, s.stm);
       }
-      launch_reduce_partial(s.dPart, g, b, s.dNorm, st);
+      launch_reduce_partial(s.dPart, g, b, s.dNorm, s.stm);
       s.resid_ready = true;
       std::swap(s.sX, s.sXn);
       std::swap(s.sAX, s.sAXn);
@@ -1970,7 +2039,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
   int rc = PC_OK;
   for (int i = 0; i < K; i++) {
     KSolve& s = ks[i];
-    cudaMemcpyAsync(s.hN + 2 * b, s.dLam, b * sizeof(double), cudaMemcpyDeviceToHost, st);
+    cudaMemcpyAsync(s.hN + 2 * b, s.dLam, b * sizeof(double), cudaMemcpyDeviceToHost, s.stm);
     if (evec_out) {
       ColPtrs X;
       MutColPtrs Y;
@@ -1979,7 +2048,7 @@ static int solve_batch(pc_ctx* c, const double* kpts, int K, int kidx0, int nev,
         Y.p[j] = evec_out + ((size_t)i * nev + j) * len;
       }
       c->launches += 1;
-      normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, st>>>(X, s.dNorm, Y, len);
+      normalize_copy_kernel<<<dim3(148 * 2, nev), 256, 0, s.stm>>>(X, s.dNorm, Y, len);
     }
   }
   CHK(sync("lobpcg"));

@@ -123,3 +123,18 @@ def test_shard_partition():
             flat = sorted(i for p in parts for i in p)
             assert flat == list(range(nk))
             assert max(len(p) for p in parts) == bands.local_capacity(nk, w)
+
+
+def test_chunk_queue_and_runs():
+    """kbatch > 1: the queue hands out chunks of consecutive k indices (lock-step batches); a chunk with a
+    gap is split into runs of consecutive indices (pc_bands keys start blocks by kindex_offset + i)."""
+    q = bands.job_queue([9, 3, 4, 5, 6, 0, 1, 2], kbatch=3)
+    got = []
+    while True:
+        ch = q.next()
+        if ch is None:
+            break
+        got.append(ch)
+    assert got == [[0, 1, 2], [3, 4, 5], [6, 9]]
+    assert bands.runs([6, 9]) == [[6], [9]]
+    assert bands.runs([3, 4, 5, 7, 8]) == [[3, 4, 5], [7, 8]]

@@ -17,7 +17,7 @@ W = synth.WORKLOADS[wname]
 kp = W.kpoints()
 idx = list(range(1, 1 + nk))
 out = {"workload": wname, "n": W.n, "nk": nk}
-for kb in (1, 4, 8, 16):
+for kb in (1, 4, 8, 12):
     ctx = api.pc_create(W.A(), W.n, W.eps1(), W.masks())
     api.pc_set_option(ctx, "kbatch", kb)
     api.pc_bands(ctx, kp[1:1 + kb], nev=W.nev, tol=1e-5)  # warm-up
