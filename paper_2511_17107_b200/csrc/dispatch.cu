@@ -12,11 +12,6 @@ PC_FFT_SIZES(PC_DECL)
                              const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st);
 PC_FFT_SIZES(PC_DECL2)
 #undef PC_DECL2
-#define PC_DECL3(N)                                                                                       \
-  cudaError_t xexg_launch_##N(const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,         \
-                              const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st);
-PC_FFT_SIZES(PC_DECL3)
-#undef PC_DECL3
 
 int fft_supported(int n) {
 #define PC_CASE(N) if (n == N) return 1;
@@ -49,16 +44,6 @@ cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out
 #define PC_SW2(N) case N: return xex_launch_##N(mode, in, out, ncols, mask, ec, tw, scale, z0, nz, st);
     PC_FFT_SIZES(PC_SW2)
 #undef PC_SW2
-    default: return cudaErrorInvalidValue;
-  }
-}
-
-cudaError_t launch_xexg(int n, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
-                        const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st) {
-  switch (n) {
-#define PC_SW3(N) case N: return xexg_launch_##N(in, out, ncols, mask, ec, tw, scale, st);
-    PC_FFT_SIZES(PC_SW3)
-#undef PC_SW3
     default: return cudaErrorInvalidValue;
   }
 }

@@ -59,19 +59,6 @@ static cudaError_t run_xex(const ColPtrs& in, const MutColPtrs& out, int ncols, 
   return cudaGetLastError();
 }
 
-cudaError_t PC_CAT(xexg_launch_, PC_FFT_N)(const ColPtrs& in, const MutColPtrs& out, int ncols,
-                                           const uint8_t* mask, const EpsCoef& ec, const cplx* tw, double scale,
-                                           cudaStream_t st) {
-  constexpr int N = PC_FFT_N;
-  using Cfg = XexgCfg<N>;
-  auto kern = xexg_kernel<N>;
-  cudaError_t e = smem_attr((const void*)kern, (int)Cfg::SMEM);
-  if (e != cudaSuccess) return e;
-  dim3 grid((N / Cfg::TP) * (N / Cfg::ZC), ncols);
-  kern<<<grid, Cfg::NT, Cfg::SMEM, st>>>(in, out, mask, ec, tw, scale);
-  return cudaGetLastError();
-}
-
 cudaError_t PC_CAT(xex_launch_, PC_FFT_N)(int mode, const ColPtrs& in, const MutColPtrs& out, int ncols,
                                           const uint8_t* mask, const EpsCoef& ec, const cplx* tw, double scale,
                                           int z0, int nz, cudaStream_t st) {

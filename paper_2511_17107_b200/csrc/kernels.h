@@ -61,11 +61,6 @@ cudaError_t launch_fft_pass(int n, int axis, int dir, int kind, const ColPtrs& i
 cudaError_t launch_xex(int n, int mode, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
                        const EpsCoef& ec, const cplx* tw, double scale, int z0, int nz, cudaStream_t st);
 
-// general CrossDoF medium (eps_13 or eps_23 != 0): x-inverse DFT + full M_eps stencil + x-forward DFT in
-// one pass (z-walking CTAs with a ring of planes, xex.cuh); in -> out (must differ)
-cudaError_t launch_xexg(int n, const ColPtrs& in, const MutColPtrs& out, int ncols, const uint8_t* mask,
-                        const EpsCoef& ec, const cplx* tw, double scale, cudaStream_t st);
-
 // fused xy-plane pass (plane2.cu, N = 128): y-inverse DFT, x-inverse DFT, M_eps (same media as
 // launch_xex), x-forward DFT, y-forward DFT of every z-plane of every column, unnormalised, in -> out
 // (must differ).  One thread-block cluster of 16 CTAs per z-plane (distributed shared memory).

@@ -674,28 +674,6 @@ static int apply_fourier(pc_ctx* c, const ColPtrs& X, const MutColPtrs& Y, const
     }
     return PC_OK;
   }
-  if (c->fuse_xex) {
-    // general CrossDoF medium (S_13 / S_23 couple z-neighbours): y-inverse, then x-inverse + M_eps +
-    // x-forward in one z-walking pass (xexg), y-forward, z + K_A + gamma K_B: 5 passes
-    {
-      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
-      CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));
-    }
-    {
-      Prof p(c, PC_STAT_EPS, st, 1, 2 * fl + 150.0 * pts, 109.0 * pts);
-      cudaError_t e = launch_xexg(n, Yc, WS, nc, c->d_mask, *op.ec, c->d_tw, 1.0, st);
-      if (e != cudaSuccess) return set_err(PC_ECUDA, std::string("xexg pass: ") + cudaGetErrorString(e));
-    }
-    {
-      Prof p(c, PC_STAT_FFT_MID, st, 1, fl, 96.0 * pts);
-      CHK(fft_pass(c, 1, -1, 0, Wc, WS, none, nc, 1.0, st));
-    }
-    {
-      Prof p(c, PC_STAT_FFT_Z_KA, st, 1, fl + 32.0 * pts, 112.0 * pts);
-      CHK(fft_pass(c, 2, -1, 2, Wc, Y, KX, nc, 1.0, st, 0, 0, op.prec, 0.0, mk));
-    }
-    return PC_OK;
-  }
   {
     Prof p(c, PC_STAT_FFT_MID, st, 2, 2 * fl, 2 * 96.0 * pts);
     CHK(fft_pass(c, 1, +1, 0, Yc, Y, none, nc, 1.0, st));

@@ -226,167 +226,3 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
     gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + k] = v;
   }, orow, false);
 }
-
-// ------------------------------------------------------------------------------------------
-// General CrossDoF medium (eps_13 or eps_23 != 0): the x-inverse DFT, the full M_eps stencil of P:664-673
-// (S_12, S_13, S_23 and their transposes; readings R4/R5) and the x-forward DFT in one pass.  S_13 and
-// S_23 couple z-neighbours, so a CTA owns TP y-rows (+1 halo row each side) of a run of ZC consecutive
-// z-planes and walks them in z with a ring of x-inverse-transformed planes: E^1, E^2 of planes z-1, z
-// and E^3 of planes z, z+1 (exactly what the stencil of plane z reads), plus the masks of z-1, z, z+1.
-// Every input plane is read and inverse-transformed once per run (the run's two halo planes twice), so
-// the pass moves ~(TP+2)/TP x 48 + 48 B per point and replaces the x-inverse, stencil and x-forward
-// passes of the 7-pass pipeline (3 HBM round trips).
-// ------------------------------------------------------------------------------------------
-#ifndef PC_XEXG_TP
-#define PC_XEXG_TP 4
-#endif
-#ifndef PC_XEXG_ZC
-#define PC_XEXG_ZC 16
-#endif
-#ifndef PC_XEXG_MINB
-#define PC_XEXG_MINB 2
-#endif
-template <int N>
-struct XexgCfg {
-  static constexpr int TP = pow2_div(N, PC_XEXG_TP);  // output rows per CTA
-  static constexpr int RW = TP + 2;              // held rows (y0-1 .. y0+TP)
-  static constexpr int ZC = pow2_div(N, PC_XEXG_ZC);  // z-planes per CTA
-  static constexpr int P = XRow<N>::P;
-  static constexpr int NT = 256;
-  static constexpr int ROWS_A = 2 * 2 * RW;      // [slot][c in {E1, E2}][r]
-  static constexpr int ROWS_B = 2 * RW;          // [slot][r] (E3)
-  static constexpr int ROWS_O = 3 * TP;          // [c][r] stencil output
-  static constexpr int PPT = (N * TP + NT - 1) / NT;
-  static constexpr size_t SMEM = (size_t)(ROWS_A + ROWS_B + ROWS_O) * P * sizeof(cplx) + (size_t)N * sizeof(cplx) +
-                                 (size_t)3 * RW * N;
-};
-
-template <int N>
-__global__ void __launch_bounds__(XexgCfg<N>::NT, PC_XEXG_MINB)
-xexg_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
-            double scale) {
-  using Cfg = XexgCfg<N>;
-  constexpr int TP = Cfg::TP, RW = Cfg::RW, ZC = Cfg::ZC, P = Cfg::P, NT = Cfg::NT, PPT = Cfg::PPT;
-  constexpr int N3 = N * N * N;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  cplx* s = reinterpret_cast<cplx*>(smem_raw);  // row i at s + i * P
-  cplx* tw = s + (Cfg::ROWS_A + Cfg::ROWS_B + Cfg::ROWS_O) * P;
-  uint8_t* mk8 = reinterpret_cast<uint8_t*>(tw + N);  // [plane slot (z mod 3)][r][x]
-  const int tid = threadIdx.x;
-  const int y0 = (blockIdx.x % (N / TP)) * TP, zs = (blockIdx.x / (N / TP)) * ZC;
-  const int col = blockIdx.y;
-  const cplx* gin = in.p[col];
-  cplx* gout = out.p[col];
-  auto rowA = [](int zz, int c, int r) { return ((zz & 1) * 2 + c) * RW + r; };
-  auto rowB = [](int zz, int r) { return Cfg::ROWS_A + (zz & 1) * RW + r; };
-  constexpr int ROW_O = Cfg::ROWS_A + Cfg::ROWS_B;
-  auto gy = [&](int r) { return (y0 - 1 + r + N) % N; };
-  auto zw = [](int zz) { return (zz % N + N) % N; };
-
-  xrow_twiddles<N>(tw, twg);
-  auto load_mask = [&](int zz) {
-    uint8_t* dst = mk8 + (((zz % 3) + 3) % 3) * RW * N;
-    for (int e = tid; e < RW * N; e += NT) dst[e] = __ldg(mask + ((long long)zw(zz) * N + gy(e / N)) * N + e % N);
-  };
-  // x-inverse DFT of the held rows of plane zz: E1, E2 into ring A (withA), E3 into ring B (withB)
-  auto load_plane = [&](int zz, bool withA, bool withB) {
-    const int na = withA ? 2 * RW : 0, npen = na + (withB ? RW : 0);
-    auto prow = [&](int pen) { return pen < na ? rowA(zz, pen / RW, pen % RW) : rowB(zz, pen - na); };
-    auto gload = [&](int pen, int j) {
-      const int c = pen < na ? pen / RW : 2, r = pen < na ? pen % RW : pen - na;
-      return ldg(gin + (long long)c * N3 + ((long long)zw(zz) * N + gy(r)) * N + j);
-    };
-    xrow_step1<N, +1, decltype(gload), decltype(prow), true>(s, tw, npen, gload, prow, false);
-    __syncthreads();
-    xrow_step2<N, +1>(s, npen, [&](int pen, int k, cplx v) { s[prow(pen) * P + k] = v; }, prow, true);
-  };
-  __syncthreads();
-  load_mask(zs - 1);
-  load_mask(zs);
-  load_mask(zs + 1);
-  load_plane(zs - 1, true, false);
-  __syncthreads();
-  load_plane(zs, true, true);
-  __syncthreads();
-  load_plane(zs + 1, false, true);
-  __syncthreads();
-
-  for (int z = zs; z < zs + ZC; z++) {
-    const uint8_t* mkm = mk8 + (((z - 1) % 3 + 3) % 3) * RW * N;
-    const uint8_t* mk0 = mk8 + ((z % 3 + 3) % 3) * RW * N;
-    const uint8_t* mkp = mk8 + (((z + 1) % 3 + 3) % 3) * RW * N;
-    auto V1 = [&](int zz, int r, int x) { return s[rowA(zz, 0, r) * P + x]; };
-    auto V2 = [&](int zz, int r, int x) { return s[rowA(zz, 1, r) * P + x]; };
-    auto V3 = [&](int zz, int r, int x) { return s[rowB(zz, r) * P + x]; };
-#pragma unroll
-    for (int t = 0; t < PPT; t++) {
-      const int e = tid + t * NT;
-      if (e >= N * TP) break;
-      const int x = e % N, r = 1 + e / N;  // held row of the output y = y0 + r - 1
-      const int xm = (x == 0) ? N - 1 : x - 1, xp = (x == N - 1) ? 0 : x + 1;
-      const uint8_t mp = mk0[r * N + x];
-      const double i1 = (mp & 1) ? 1.0 : 0.0, i2 = (mp & 2) ? 1.0 : 0.0, i3 = (mp & 4) ? 1.0 : 0.0;
-      auto I = [](const uint8_t* m, int rr, int xx, int bit) { return (m[rr * N + xx] >> bit) & 1 ? 1.0 : 0.0; };
-      cplx w1 = (1.0 + ec.d[0] * i1) * V1(z, r, x);
-      cplx w2 = (1.0 + ec.d[1] * i2) * V2(z, r, x);
-      cplx w3 = (1.0 + ec.d[2] * i3) * V3(z, r, x);
-      {  // S_12 v2 into w1: q in {x-1, x} x {y, y+1}, weight I1(p) + I2(q); S_12^T v1 into w2
-        cplx a = mk(0, 0), a2 = mk(0, 0);
-        const int qa[2] = {xm, x}, qb[2] = {x, xp};
-#pragma unroll
-        for (int u = 0; u < 2; u++)
-#pragma unroll
-          for (int b = 0; b < 2; b++) {
-            a = a + (i1 + I(mk0, r + b, qa[u], 1)) * V2(z, r + b, qa[u]);
-            a2 = a2 + (i2 + I(mk0, r - 1 + b, qb[u], 0)) * V1(z, r - 1 + b, qb[u]);
-          }
-        w1 = w1 + 0.125 * cmul(ec.e[0], a);
-        w2 = w2 + 0.125 * cmul(conjg(ec.e[0]), a2);
-      }
-      {  // S_13 v3 into w1: q in {x-1, x} x {z, z+1}, weight I1(p) + I3(q); S_13^T v1 into w3: {x, x+1} x {z-1, z}
-        cplx a = mk(0, 0), a2 = mk(0, 0);
-        const int qa[2] = {xm, x}, qb[2] = {x, xp};
-#pragma unroll
-        for (int u = 0; u < 2; u++) {
-          a = a + (i1 + I(mk0, r, qa[u], 2)) * V3(z, r, qa[u]) + (i1 + I(mkp, r, qa[u], 2)) * V3(z + 1, r, qa[u]);
-          a2 = a2 + (i3 + I(mkm, r, qb[u], 0)) * V1(z - 1, r, qb[u]) + (i3 + I(mk0, r, qb[u], 0)) * V1(z, r, qb[u]);
-        }
-        w1 = w1 + 0.125 * cmul(ec.e[1], a);
-        w3 = w3 + 0.125 * cmul(conjg(ec.e[1]), a2);
-      }
-      {  // S_23 v3 into w2: q in {y-1, y} x {z, z+1}, weight I2(p) + I3(q); S_23^T v2 into w3: {y, y+1} x {z-1, z}
-        cplx a = mk(0, 0), a2 = mk(0, 0);
-#pragma unroll
-        for (int b = 0; b < 2; b++) {
-          a = a + (i2 + I(mk0, r - 1 + b, x, 2)) * V3(z, r - 1 + b, x) + (i2 + I(mkp, r - 1 + b, x, 2)) * V3(z + 1, r - 1 + b, x);
-          a2 = a2 + (i3 + I(mkm, r + b, x, 1)) * V2(z - 1, r + b, x) + (i3 + I(mk0, r + b, x, 1)) * V2(z, r + b, x);
-        }
-        w2 = w2 + 0.125 * cmul(ec.e[2], a);
-        w3 = w3 + 0.125 * cmul(conjg(ec.e[2]), a2);
-      }
-      s[(ROW_O + 0 * TP + r - 1) * P + x] = scale * w1;
-      s[(ROW_O + 1 * TP + r - 1) * P + x] = scale * w2;
-      s[(ROW_O + 2 * TP + r - 1) * P + x] = scale * w3;
-    }
-    __syncthreads();
-    // forward x-DFT of the output rows, the last step writes HBM
-    {
-      auto orow = [](int pen) { return ROW_O + pen; };
-      auto sload = [&](int pen, int j) { return s[orow(pen) * P + j]; };
-      xrow_step1<N, -1, decltype(sload), decltype(orow), true>(s, tw, 3 * TP, sload, orow, true);
-      xrow_step2<N, -1>(s, 3 * TP, [&](int pen, int k, cplx v) {
-        const int c = pen / TP, r = pen % TP;
-        gout[(long long)c * N3 + ((long long)z * N + y0 + r) * N + k] = v;
-      }, orow, false);
-    }
-    if (z + 1 < zs + ZC) {
-      // next plane: E1, E2 of z+1 replace those of z-1; E3 of z+2 replaces that of z; mask of z+2
-      __syncthreads();
-      load_mask(z + 2);
-      load_plane(z + 1, true, false);
-      __syncthreads();
-      load_plane(z + 2, false, true);
-      __syncthreads();
-    }
-  }
-}
