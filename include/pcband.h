@@ -201,6 +201,12 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  vectors (default 1e-10)
  *   "p_restart"    1 (default): drop the P block when the basis is numerically rank deficient
  *   "verbose"      1: per-iteration residuals on stderr
+ *   "kbatch"       1 (default): pc_bands solves its k-points one after another; K in 2..16: in lock-step
+ *                  batches of K: one multi-k operator apply and two host synchronisations per
+ *                  LOBPCG iteration for the whole batch, each k-point's Gram / Rayleigh-Ritz / update on
+ *                  its own stream; same results as kbatch 1 (the i-th k-point of a call is still keyed by
+ *                  kindex_offset + i).  K x (nev + guard) <= 192; ignored with warm_start or precond = 1.
+ *                  Pays at n <= 32 (C2: 104 vs 27 k-points/s), equal at n = 64 to concurrent contexts
  *   "warm_start"   1: start each k-point (k != 0) from the Ritz block of the previous pc_bands
  *                  k-point solved on this context (path continuation, not in the
  *                  paper); 0 (default): cold start.  Setting the option forgets the stored block.
@@ -221,6 +227,8 @@ int pc_info(const pc_ctx *ctx, int *hpd_flags, size_t *ws_bytes_per_col);
  *                  update launches and a separate residual pass
  *   "update_tmap"  1 (default): block-update kernel with TMA tensor-copy row tiles in a 2-stage
  *                  ring (update_tmap.cu); 0: per-thread cp.async tiles (update_all.cu)
+ *   "gram_narrow"  1 (default): 8/16-column block shapes for narrow Gram products (tail iterations);
+ *                  0: the wide shapes only (process-wide)
  *   "jacobi_tol"   rotation threshold of the Rayleigh-Ritz Jacobi sweeps, |a_pq| <= tol sqrt(|a_pp a_qq|)
  *                  (process-wide; default 1e-16)
  */
