@@ -29,7 +29,10 @@ struct XexCfg {
   static constexpr int TP = pow2_div(N, PC_XEX_TP);   // output rows per tile
   static constexpr int RP = TP + 2;           // rows held (1 halo row each side)
   static constexpr int P = XRow<N>::P;        // row pitch in complex
-  static constexpr int NT = 256;
+#ifndef PC_XEX_NT
+#define PC_XEX_NT 256
+#endif
+  static constexpr int NT = PC_XEX_NT;
   static constexpr int PPT = (N * TP + NT - 1) / NT;  // stencil points per thread
   static constexpr size_t SMEM = (size_t)3 * RP * P * sizeof(cplx) + (size_t)N * sizeof(cplx) + (size_t)RP * N;
 };

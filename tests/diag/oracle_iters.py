@@ -20,8 +20,12 @@ ap.add_argument("workload")
 ap.add_argument("kidx", type=int, nargs="+")
 ap.add_argument("--tol", type=float, default=1e-5)
 ap.add_argument("--out", default=None)
+ap.add_argument("--n", type=int, default=0, help="grid size override (same lattice, geometry, eps1, path)")
 a = ap.parse_args()
 W = synth.WORKLOADS[a.workload]
+if a.n:
+    import dataclasses
+    W = dataclasses.replace(W, n=a.n)
 rows = []
 for ki in a.kidx:
     k = W.kpoints()[ki]
@@ -32,7 +36,7 @@ for ki in a.kidx:
     rows.append({"kidx": ki, "k": k.tolist(), "tol": a.tol, "guard": 5, "iterations": info["iterations"],
                  "seconds": time.time() - t0, "omega2": ev.tolist(), "max_res": float(res.max())})
     print(json.dumps(rows[-1]), flush=True)
-out = {"workload": a.workload, "n": W.n, "nev": W.nev, "solver": "oracle eigs_iterative (SciPy LOBPCG, oracle K_P^-1)",
+out = {"workload": a.workload, "n": W.n, "grid_override": bool(a.n), "nev": W.nev, "solver": "oracle eigs_iterative (SciPy LOBPCG, oracle K_P^-1)",
        "threads": os.environ.get("OMP_NUM_THREADS"), "rows": rows}
 if a.out:
     with open(a.out, "w") as f:

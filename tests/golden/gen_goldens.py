@@ -77,15 +77,31 @@ def run_set(name, kidx, jobs, tol=None):
         for ki, k, ev, res, its, sec in ex.map(_solve, [(wname, i, tol, maxiter) for i in kidx]):
             done[ki] = (k, ev, res, its, sec)
             print(f"{name} k{ki} its={its} {sec:.0f}s maxres={res.max():.2e} ev={ev}", flush=True)
+    # merge: rows of k-points not recomputed here are kept from an existing file (one file per set)
+    old_rows, old_cmds = {}, []
+    if os.path.exists(path):
+        for line in open(path):
+            if line.startswith("# Command:"):
+                old_cmds.append(line.rstrip("\n"))
+            elif line.strip() and not line.startswith("#"):
+                key = line.split()[0]
+                ki = int(key.lstrip("kevrsit")) if key[0] in "kers" or key.startswith("its") else None
+                if ki is not None and ki not in done:
+                    old_rows.setdefault(ki, []).append(line)
     with open(path, "w") as f:
         f.write(f"# {wname}: {w.lattice.upper()} {w.geometry}, eps1 '{w.eps}', n = {w.n}, {w.nev} smallest "
                 f"eigenvalues of the penalised operator (PAPER.md:259, gamma rule P:457-462), CrossDoF.\n")
         f.write("# Source: oracle/pc_oracle.py eigs_iterative (SciPy LOBPCG on the oracle's sparse operator,\n"
-                f"#   oracle K_P^-1 preconditioner, guard 5, tol {tol:g} absolute Res_j, P:1059-1064).\n")
-        f.write(f"# Command: python tests/golden/gen_goldens.py {name} --k {','.join(map(str, kidx))}"
+                "#   oracle K_P^-1 preconditioner, guard 5, absolute Res_j tolerance as in each command, P:1059-1064).\n")
+        for oc in old_cmds:
+            f.write(oc + "\n")
+        f.write(f"# Command: python tests/golden/gen_goldens.py {name} --k {','.join(map(str, kidx))} --tol {tol:g}"
                 f"   git {_git()}   {time.strftime('%Y-%m-%d')}\n")
         f.write("# Rows: k<i> = k-point index on synth.kpath(lattice, 8) then kx ky kz; ev<i> = eigenvalues;\n"
                 "#       res<i> = final oracle residual norms; its<i> = SciPy LOBPCG iterations.\n")
+        for ki in sorted(old_rows):
+            for line in old_rows[ki]:
+                f.write(line)
         for ki in sorted(done):
             k, ev, res, its, _ = done[ki]
             f.write(f"k{ki} " + " ".join(f"{v:.17g}" for v in k) + "\n")

@@ -395,3 +395,25 @@ def test_bands_kbatch_equals_single(api, wname, kb, idx):
     for t, ki in enumerate(idx):
         if f"ev{ki}" in g:
             assert rel(r["omega2"][t], g[f"ev{ki}"]) <= 1e-8
+
+
+def test_bands_kbatch_eigenvectors(api):
+    """Lock-step batch with eigenvector output (k-major, one block per k-point): every
+    returned pair is an eigenpair of the oracle operator of its own k, including k = 0."""
+    n, A = 8, synth.lattice("fcc")
+    e = synth.eps_pseudochiral()
+    masks = synth.make_masks("random", A, n, seed=12)
+    ctx = api.pc_create(A, n, e, masks)
+    kp = np.array([[0.4, 1.0, -0.3], [0.0, 0.0, 0.0], [PI, PI, PI]])
+    api.pc_set_option(ctx, "kbatch", 3)
+    ev = torch.empty(3 * 6, 3 * n ** 3, dtype=torch.complex128, device="cuda")
+    r = api.pc_bands(ctx, kp, nev=6, tol=1e-9, evecs=ev)
+    assert (r["status"] == 0).all()
+    V = ev.cpu().numpy()
+    for i, k in enumerate(kp):
+        op = O.PenalizedOperator(n, k, A, e, masks)
+        Vi = V[6 * i:6 * (i + 1)]
+        res = np.linalg.norm(op.apply_fourier(Vi) - r["omega2"][i][:, None] * Vi, axis=1)
+        assert np.allclose(np.linalg.norm(Vi, axis=1), 1.0, atol=1e-12)
+        assert res.max() <= 1e-8
+        assert rel(r["omega2"][i], O.eigs_dense(op, 6)) <= 1e-8
