@@ -153,7 +153,10 @@ def oracle_iters(W):
     if not d or not d.get("rows"):
         return None, None
     its = [r["iterations"] for r in d["rows"]]
-    return float(np.mean(its)), f"profiles/oracle_iters_{W.name.lower()}.json ({d['rows'][0]['tol']:g}, k {[r['kidx'] for r in d['rows']]})"
+    grid = f", measured on the n = {d['n']} grid of the same geometry (the count barely depends on n: the device " \
+           f"needs 82 / 85 / 89 at n = 32 / 64 / 128)" if d.get("grid_override") else ""
+    return float(np.mean(its)), (f"profiles/oracle_iters_{W.name.lower()}.json: tol {d['rows'][0]['tol']:g}, "
+                                 f"k {[r['kidx'] for r in d['rows']]}, iterations {its}{grid}")
 
 
 def oracle_worker(args):
