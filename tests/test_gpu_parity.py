@@ -298,8 +298,10 @@ def test_identity_selftest_full_size(api, lat, n):
 
 
 # ------------------------------------------------------------------------------------- Jacobi
-@pytest.mark.parametrize("n", [1, 2, 5, 16, 45, 75, 80])
+@pytest.mark.parametrize("n", [1, 2, 5, 16, 36, 45, 75, 80])
 def test_device_jacobi_eigh(api, n):
+    """The Rayleigh-Ritz eigensolver (one-CTA cyclic Jacobi) against numpy on Hermitian matrices with
+    spectra over 7 decades, a degenerate cluster and a diagonal matrix."""
     rng = np.random.default_rng(n)
     M = rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))
     M = M + M.conj().T
@@ -312,6 +314,15 @@ def test_device_jacobi_eigh(api, n):
     assert np.allclose(w, wr, rtol=1e-12, atol=1e-12 * np.abs(wr).max())
     assert np.allclose(V.conj().T @ V, np.eye(n), atol=1e-12)
     assert np.linalg.norm(M @ V - V * w[None, :]) <= 1e-12 * np.linalg.norm(M)
+    # a degenerate cluster (as at symmetry points) and a diagonal matrix (all rotations trivial)
+    if n >= 5:
+        D = np.diag(np.r_[np.full(3, 2.0), np.arange(n - 3) + 3.0]).astype(complex)
+        Qr, _ = np.linalg.qr(rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n)))
+        for Mx in (Qr @ D @ Qr.conj().T, D):
+            Mx = 0.5 * (Mx + Mx.conj().T)
+            w2, V2, _ = api.pc_debug_heevj(Mx)
+            assert np.allclose(w2, np.linalg.eigvalsh(Mx), atol=1e-12 * n)
+            assert np.allclose(V2.conj().T @ V2, np.eye(n), atol=1e-12)
 
 
 @pytest.mark.parametrize("eps,mode,n", [("pc", "crossdof", 16), ("iso", "crossdof", 12), ("sdd", "trivial", 8),
