@@ -413,6 +413,7 @@ extern "C" void pc_destroy(pc_ctx* c) {
   auto t0 = now();
   cudaSetDevice(c->device);
   if (c->stream) cudaStreamSynchronize(c->stream);
+  for (auto s_ : c->bst) cudaStreamSynchronize(s_);  // batch streams (an error return can leave work queued)
   prof_flush(c);
   for (auto e : c->ev_pool) cudaEventDestroy(e);
   auto t1 = now();
