@@ -2061,7 +2061,11 @@ extern "C" int pc_bands(pc_ctx* c, const double* kpts, int nk, int nev, double t
                            omega2 + (size_t)i0 * nev, resid ? resid + (size_t)i0 * nev : nullptr,
                            iters ? iters + i0 : nullptr, status ? status + i0 : nullptr,
                            evecs ? reinterpret_cast<cplx*>(evecs) + (size_t)i0 * nev * c->len : nullptr);
-      if (rc < 0) return rc;
+      if (rc < 0) {  // leave no batch work queued behind an error
+        for (auto s_ : c->bst) cudaStreamSynchronize(s_);
+        cudaStreamSynchronize(c->stream);
+        return rc;
+      }
       if (rc == PC_ENOTCONV) rc_all = PC_ENOTCONV;
     }
     return rc_all;
