@@ -49,6 +49,9 @@ DEV void xrow_twiddles(cplx* tw, const cplx* __restrict__ twg) {
   for (int j = threadIdx.x; j < N; j += blockDim.x) tw[j] = ldg(twg + ((j % R2) * (j / R2)) % N);
 }
 
+#ifndef PC_XEX_TWREC
+#define PC_XEX_TWREC 1
+#endif
 template <int N, int DIR, class Load, class Row, bool TT = false>
 DEV void xrow_step1(cplx* s, const cplx* tw, int npen, Load load, Row row, bool sync_inplace) {
   using X = XRow<N>;
@@ -67,11 +70,36 @@ DEV void xrow_step1(cplx* s, const cplx* tw, int npen, Load load, Row row, bool 
     if (sync_inplace) __syncthreads();
     if (act) {
       cplx* d = s + row(pen) * P + j2 * S1;
+      if constexpr (TT && PC_XEX_TWREC && R1 % 4 == 0 && R1 >= 8) {
+        // twiddles W^{j2 k1}, k1 = 4a + b, from two table reads (W^{j2}, W^{4 j2}) and at most 3 + R1/4
+        // products (<= 4 roundings each): the 16-B twiddle reads were as many shared-memory wavefronts
+        // as the data of this step
+        cplx w1 = tw[1 * R2 + j2], w4 = tw[4 * R2 + j2];
+        if (DIR > 0) {
+          w1.y = -w1.y;
+          w4.y = -w4.y;
+        }
+        const cplx w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+        cplx wa = mk(1.0, 0.0);
 #pragma unroll
-      for (int k1 = 0; k1 < R1; k1++) {
-        cplx w = TT ? tw[k1 * R2 + j2] : tw[(j2 * k1) % N];
-        if (DIR > 0) w.y = -w.y;
-        d[k1] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+        for (int a = 0; a < R1 / 4; a++) {
+          if (a == 1) wa = w4;
+          if (a > 1) wa = cmul(wa, w4);
+#pragma unroll
+          for (int b = 0; b < 4; b++) {
+            const int k1 = 4 * a + b;
+            cplx w = (b == 0) ? wa : (b == 1) ? w1 : (b == 2) ? w2 : w3;
+            if (a > 0 && b > 0) w = cmul(wa, w);
+            d[k1] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+          }
+        }
+      } else {
+#pragma unroll
+        for (int k1 = 0; k1 < R1; k1++) {
+          cplx w = TT ? tw[k1 * R2 + j2] : tw[(j2 * k1) % N];
+          if (DIR > 0) w.y = -w.y;
+          d[k1] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+        }
       }
     }
     if (sync_inplace) __syncthreads();
@@ -106,6 +134,9 @@ DEV void xrow_step2(const cplx* s, int npen, Store store, Row row, bool sync_inp
 }
 
 // MODE: 0 diagonal, 1 crossdof with only eps_12, 2 trivial
+#ifndef PC_XEX_COLS
+#define PC_XEX_COLS 1
+#endif
 #ifndef PC_XEX_MINB
 #define PC_XEX_MINB 2
 #endif
@@ -127,10 +158,15 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   cplx* gout = out.p[col];
 
   // Rows held per component (smem row r <-> y = y0 - 1 + r, r = 0 .. TP+1).  Only S_12 needs the halo
-  // rows (E^1 at y0-1, E^2 at y0+TP); in MODE 1 all three components hold all RP rows so the pencil
-  // list is uniform (pencil = smem row c*RP + r).
-  constexpr int NPEN = (MODE == 1) ? 3 * RP : 3 * TP;
-  auto prow = [](int pen) { return (MODE == 1) ? pen : (pen / TP) * RP + 1 + pen % TP; };
+  // rows (E^1 at y0-1, E^2 at y0+TP).  MODE 1 holds only the halo rows S_12 reads: E^1 rows r = 0..TP, E^2 rows r = 1..TP+1, E^3 rows
+  // r = 1..TP (3 TP + 2 pencils instead of 3 TP + 6).
+  constexpr int NPEN = (MODE == 1) ? 3 * TP + 2 : 3 * TP;
+  auto prow = [](int pen) {
+    if (MODE != 1) return (pen / TP) * RP + 1 + pen % TP;
+    if (pen <= TP) return pen;
+    if (pen <= 2 * TP + 1) return RP + (pen - TP);
+    return 2 * RP + 1 + (pen - 2 * TP - 2);
+  };
   auto grow = [&](int row) {  // global offset of smem row
     const int c = row / RP, r = row % RP;
     const int y = (y0 - 1 + r + N) % N;
@@ -161,13 +197,26 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   if constexpr (N % 16 == 0) cp_async_wait<0>();
   __syncthreads();
 
-  // M_eps on the TP output rows (registers first: the stencil reads neighbours)
+  // M_eps on the TP output rows (registers first: the stencil reads neighbours).  COLS: each thread
+  // takes PPT consecutive rows of one x, so the rows its stencils share are read from shared memory once
+  // (6 instead of 9 field reads per point in MODE 1).
+  constexpr bool COLS = PC_XEX_COLS && NT % N == 0 && PPT * NT == N * TP;
+  auto spt = [&](int t, int& x, int& r) {
+    if (COLS) {
+      x = tid % N;
+      r = 1 + (tid / N) * PPT + t;
+      return true;
+    }
+    const int e = tid + t * NT;
+    x = e % N;
+    r = 1 + e / N;
+    return e < N * TP;
+  };
   cplx w[PPT][3];
 #pragma unroll
   for (int t = 0; t < PPT; t++) {
-    const int e = tid + t * NT;
-    if (e >= N * TP) break;
-    const int x = e % N, r = 1 + e / N;
+    int x, r;
+    if (!spt(t, x, r)) break;
     const uint8_t mp = mk8[r * N + x];
     const double i1 = (mp & 1) ? 1.0 : 0.0, i2 = (mp & 2) ? 1.0 : 0.0, i3 = (mp & 4) ? 1.0 : 0.0;
     const cplx v1 = s[(0 * RP + r) * P + x], v2 = s[(1 * RP + r) * P + x], v3 = s[(2 * RP + r) * P + x];
@@ -212,9 +261,8 @@ xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef
   __syncthreads();
 #pragma unroll
   for (int t = 0; t < PPT; t++) {
-    const int e = tid + t * NT;
-    if (e >= N * TP) break;
-    const int x = e % N, r = 1 + e / N;
+    int x, r;
+    if (!spt(t, x, r)) break;
 #pragma unroll
     for (int c = 0; c < 3; c++) s[(c * RP + r) * P + x] = w[t][c];
   }
