@@ -1,0 +1,6 @@
+mkdir -p gpurun_out/s30
+timeout 2400 python -m pytest tests -m gpu -q > gpurun_out/s30/pytest_gpu.log 2>&1; echo "rc $?" >> gpurun_out/s30/pytest_gpu.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke(); print('smoke ok')" > gpurun_out/s30/smoke.log 2>&1
+timeout 900 python bench.py > gpurun_out/s30/bench.json 2> gpurun_out/s30/bench.err
+timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 1500 --csv --log-file gpurun_out/s30/launches_bench.csv python bench.py --steps 1 --warmup 3 --streams 1 --e2e-steps 0 --no-cpu-baseline --no-alt > gpurun_out/s30/ncu_launch.log 2>&1
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:"update_tmap|gram_kernel|xex_kernel|fft_pass_kernel" -s 12 -c 10 -o gpurun_out/s30/lobpcg python tools/prof_lobpcg.py --maxit 12 > gpurun_out/s30/ncu_full.log 2>&1
