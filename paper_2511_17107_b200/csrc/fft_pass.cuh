@@ -77,7 +77,12 @@ struct TileCfg {
   static constexpr int NT = TP * FftPlan<N>::R1;
   // x pass: [c][p][j] with pitch N+1 (tile rows contiguous as in HBM: conflict-free cp.async writes);
   // y/z passes: [c][j][p] with pitch TP+1.  Both odd pitches: conflict-free 16-B fragment accesses.
-  static constexpr int SPAN = (TP * (N + 1) > N * TPP) ? TP * (N + 1) : N * TPP;
+  // (C = 3 tiles are z-pass tiles only: N * TPP, which keeps the symbol passes at 56 KB = 4 CTAs/SM)
+#ifndef PC_ZSPAN_TIGHT
+#define PC_ZSPAN_TIGHT 1
+#endif
+  static constexpr int SPAN =
+      (C == 3 && PC_ZSPAN_TIGHT) ? N * TPP : (TP * (N + 1) > N * TPP) ? TP * (N + 1) : N * TPP;
   // C = 1: persistent CTAs with a 2-stage prefetch pipeline; C = 3 (fused symbol passes, 3x the tile):
   // one tile per CTA and higher occupancy instead
 #ifndef PC_C3_STAGES
@@ -126,18 +131,22 @@ struct TileMap {
 #define PC_KAG_PREFETCH 0  // 1: last pass loads g before the DFTs (see fft_pass_kernel)
 #endif
 #ifndef PC_FFT_BOUNDS
-#define PC_FFT_BOUNDS 0  // 1: min-blocks launch bounds (4 CTAs/SM for the symbol passes, 3 for the plain ones)
+#define PC_FFT_BOUNDS 1
 #endif
+// N <= 128: plain passes at most 85 registers so that 3 persistent CTAs of 256 threads fit an SM (86
+// registers left 2: the y pass at n = 128 ran 5 % slower); symbol passes at most 128 (4 CTAs of 128
+// threads).  Larger N: no minimum (0 = unspecified; the caps spill there).
 #if PC_FFT_BOUNDS
-#define PC_FFT_LB(OP_, ...) __launch_bounds__((__VA_ARGS__), (OP_) != OP_NONE ? 4 : 3)
+#define PC_FFT_LB(N_, OP_, ...) __launch_bounds__((__VA_ARGS__), ((N_) <= 128) ? ((OP_) != OP_NONE ? 4 : 3) : 0)
 #else
-#define PC_FFT_LB(OP_, ...) __launch_bounds__((__VA_ARGS__))
+#define PC_FFT_LB(N_, OP_, ...) __launch_bounds__((__VA_ARGS__))
 #endif
 template <int N, int AXIS, int DIR, int OP, int C>
-__global__ void PC_FFT_LB(OP, TileCfg<N, C>::NT)
+__global__ void PC_FFT_LB(N, OP, TileCfg<N, C>::NT)
 fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) {
   constexpr int R1 = FftPlan<N>::R1, R2 = FftPlan<N>::R2;
   static_assert(R1 * R2 == N, "bad plan");
+  static_assert(C == 1 || AXIS == 2, "3-component tiles are z-pass tiles");
   constexpr int TP = TileCfg<N, C>::TP, TPP = TileCfg<N, C>::TPP, NT = TileCfg<N, C>::NT;
   constexpr int SPAN = TileCfg<N, C>::SPAN;
   constexpr int N3 = N * N * N;
