@@ -12,7 +12,13 @@
 #include "kernels.h"
 
 constexpr int RR_MAXN = 80;
-constexpr int RR_THREADS = 512;
+#ifndef PC_RR_THREADS
+#define PC_RR_THREADS 1024
+#endif
+constexpr int RR_THREADS = PC_RR_THREADS;
+#ifndef PC_RR_EARLY
+#define PC_RR_EARLY 1
+#endif
 
 struct JacSm {
   int P[RR_MAXN / 2], Q[RR_MAXN / 2];
@@ -29,13 +35,21 @@ DEV void tpair(int r, int i, int m, int& P, int& Q) {
 }
 
 // A, V column-major with leading dimension ld (= np).  A Hermitian n x n zero-padded to np (even).
+// One round: the h = np/2 rotations (one thread each), one barrier, then the h^2 two-sided 2x2 block
+// updates of A and the np*h row updates of V as one parallel loop (<= 2 items per thread at np <= 64
+// with 1024 threads), one barrier.  Stops after a sweep without rotations, or (PC_RR_EARLY) after a
+// sweep whose largest relative off-diagonal |a_pq|^2 / |a_pp a_qq| was below max(1e-16, tol^2): cyclic
+// Jacobi converges quadratically, so what that sweep leaves is O(1e-16) relative -- the sweep after it
+// would only remove rotations at the rounding level.
 DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps, double rel_tol = 1e-16) {
   const int tid = threadIdx.x;
   const int h = np / 2;
   const double tol2 = rel_tol * rel_tol;
+  const double stop2 = fmax(1e-16, tol2);
   int sweep = 0;
   for (; sweep < max_sweeps; sweep++) {
-    int swept = 0;  // any rotation in this sweep (CTA-uniform)
+    int swept = 0;     // any rotation in this sweep (CTA-uniform)
+    int big = 0;       // this thread saw a rotation with ratio^2 > stop2 in this sweep
     for (int r = 0; r < np - 1; r++) {
       int rot = 0;
       for (int i = tid; i < h; i += blockDim.x) {
@@ -50,7 +64,8 @@ DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_
           const cplx apq = A[P + Q * ld];
           const double m2 = fma(apq.x, apq.x, apq.y * apq.y);
           const double app = A[P + P * ld].x, aqq = A[Q + Q * ld].x;
-          if (m2 > 0.0 && m2 > tol2 * fabs(app * aqq)) {
+          const double dd = fabs(app * aqq);
+          if (m2 > 0.0 && m2 > tol2 * dd) {
             const double rm = rsqrt(m2);
             const double z = 0.5 * (aqq - app) * rm;
             const double t = copysign(1.0, z) / (fabs(z) + sqrt(fma(z, z, 1.0)));
@@ -58,45 +73,88 @@ DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_
             s = t * c;
             e = mk(apq.x * rm, apq.y * rm);
             rot = 1;
+            big |= !(m2 <= stop2 * dd);
           }
         }
         js.P[i] = P; js.Q[i] = Q; js.c[i] = c; js.s[i] = s; js.e[i] = e;
       }
       swept |= __syncthreads_or(rot);
-      for (int it = tid; it < h * h; it += blockDim.x) {
-        const int i = it % h, i2 = it / h;
-        const double c = js.c[i], s = js.s[i], c2 = js.c[i2], s2 = js.s[i2];
-        if (s == 0.0 && s2 == 0.0) continue;
-        const int P = js.P[i], Q = js.Q[i], P2 = js.P[i2], Q2 = js.Q[i2];
-        const cplx e = js.e[i], e2 = js.e[i2];
-        cplx m00 = A[P + P2 * ld], m01 = A[P + Q2 * ld], m10 = A[Q + P2 * ld], m11 = A[Q + Q2 * ld];
-        // L = U_i^H M
-        cplx se = s * e, sec = s * conjg(e);
-        cplx l00 = c * m00 - cmul(se, m10), l01 = c * m01 - cmul(se, m11);
-        cplx l10 = cmul(sec, m00) + c * m10, l11 = cmul(sec, m01) + c * m11;
-        // R = L U_i2
-        cplx se2 = s2 * e2, sec2 = s2 * conjg(e2);
-        A[P + P2 * ld] = c2 * l00 - cmul(sec2, l01);
-        A[P + Q2 * ld] = cmul(se2, l00) + c2 * l01;
-        A[Q + P2 * ld] = c2 * l10 - cmul(sec2, l11);
-        A[Q + Q2 * ld] = cmul(se2, l10) + c2 * l11;
-      }
-      for (int it = tid; it < np * h; it += blockDim.x) {
-        const int j = it % np, i = it / np;
-        const double s = js.s[i];
-        if (s == 0.0) continue;
-        const double c = js.c[i];
-        const int P = js.P[i], Q = js.Q[i];
-        const cplx e = js.e[i];
-        cplx a = V[j + P * ld], b = V[j + Q * ld];
-        V[j + P * ld] = c * a - cmul(s * conjg(e), b);
-        V[j + Q * ld] = cmul(s * e, a) + c * b;
+      const int na = h * h, nitem = na + np * h;
+      for (int it = tid; it < nitem; it += blockDim.x) {
+        if (it < na) {
+          const int i = it % h, i2 = it / h;
+          const double c = js.c[i], s = js.s[i], c2 = js.c[i2], s2 = js.s[i2];
+          if (s == 0.0 && s2 == 0.0) continue;
+          const int P = js.P[i], Q = js.Q[i], P2 = js.P[i2], Q2 = js.Q[i2];
+          const cplx e = js.e[i], e2 = js.e[i2];
+          cplx m00 = A[P + P2 * ld], m01 = A[P + Q2 * ld], m10 = A[Q + P2 * ld], m11 = A[Q + Q2 * ld];
+          // L = U_i^H M
+          cplx se = s * e, sec = s * conjg(e);
+          cplx l00 = c * m00 - cmul(se, m10), l01 = c * m01 - cmul(se, m11);
+          cplx l10 = cmul(sec, m00) + c * m10, l11 = cmul(sec, m01) + c * m11;
+          // R = L U_i2
+          cplx se2 = s2 * e2, sec2 = s2 * conjg(e2);
+          A[P + P2 * ld] = c2 * l00 - cmul(sec2, l01);
+          A[P + Q2 * ld] = cmul(se2, l00) + c2 * l01;
+          A[Q + P2 * ld] = c2 * l10 - cmul(sec2, l11);
+          A[Q + Q2 * ld] = cmul(se2, l10) + c2 * l11;
+        } else {
+          const int iv = it - na, j = iv % np, i = iv / np;
+          const double s = js.s[i];
+          if (s == 0.0) continue;
+          const double c = js.c[i];
+          const int P = js.P[i], Q = js.Q[i];
+          const cplx e = js.e[i];
+          cplx a = V[j + P * ld], b = V[j + Q * ld];
+          V[j + P * ld] = c * a - cmul(s * conjg(e), b);
+          V[j + Q * ld] = cmul(s * e, a) + c * b;
+        }
       }
       __syncthreads();
     }
     if (!swept) break;
+    if (PC_RR_EARLY && !__syncthreads_or(big)) {
+      sweep++;
+      break;
+    }
   }
   return sweep;
+}
+
+// Triangular solves with many right-hand sides, one warp per column c (lanes own rows lane + 32 q),
+// column-sweep order without barriers: y_i = b_i / t_ii (dinv[i] = 1 / t_ii), broadcast from the owner
+// lane, then b_m -= t_mi y_i for the rows still to solve.  T lower (forward, i = 0..p-1) or upper
+// (backward, i = p-1..0), column-major in shared memory (ld), so a step reads T's column i: consecutive
+// rows over the lanes.  B column c comes from bfun(m, c); yfun(i, c, y) stores y_i (owner lane).
+constexpr int RR_RPL = (RR_MAXN + 31) / 32;
+template <bool UPPER, class BF, class YF>
+DEV void tri_solve_cols(const cplx* T, int ld, const double* dinv, int p, int ncol, BF bfun, YF yfun) {
+  const int lane = threadIdx.x & 31, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x >> 5; c < ncol; c += nw) {
+    cplx b[RR_RPL];
+#pragma unroll
+    for (int q = 0; q < RR_RPL; q++) {
+      const int m = lane + 32 * q;
+      b[q] = (m < p) ? bfun(m, c) : mk(0.0, 0.0);
+    }
+    for (int st = 0; st < p; st++) {
+      const int i = UPPER ? p - 1 - st : st;
+      const int qi = i >> 5, li = i & 31;
+      cplx bi = b[0];
+#pragma unroll
+      for (int q = 1; q < RR_RPL; q++)
+        if (qi == q) bi = b[q];
+      cplx y = dinv[i] * bi;
+      y.x = __shfl_sync(0xffffffffu, y.x, li);
+      y.y = __shfl_sync(0xffffffffu, y.y, li);
+      if (lane == li) yfun(i, c, y);
+#pragma unroll
+      for (int q = 0; q < RR_RPL; q++) {
+        const int m = lane + 32 * q;
+        if (UPPER ? (m < i) : (m > i && m < p)) b[q] = b[q] - cmul(T[m + i * ld], y);
+      }
+    }
+  }
 }
 
 // rank[i] = position of w[i] in ascending order (ties by index); valid for i < n
@@ -146,7 +204,7 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   cplx* A = reinterpret_cast<cplx*>(rsm);
   cplx* V = A + np * np;
   __shared__ JacSm js;
-  __shared__ double dsc[RR_MAXN], sig[RR_MAXN];
+  __shared__ double dsc[RR_MAXN], sig[RR_MAXN], dinv[RR_MAXN];
   __shared__ int keep[RR_MAXN], order[RR_MAXN];
   __shared__ int rank_sh, chol_flag;
   const int tid = threadIdx.x;
@@ -186,26 +244,16 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   int r = p;
   int rp = np;
   if (chol) {
-    // Z = L^{-1} (D G_A D) by forward substitution, row by row, into V (smem, ld)
-    for (int i = 0; i < p; i++) {
-      const double inv = 1.0 / A[i + i * ld].x;
-      for (int j = tid; j < p; j += blockDim.x) {
-        cplx acc = (dsc[i] * dsc[j]) * GA[i + (size_t)j * p];
-        for (int k = 0; k < i; k++) acc = acc - cmul(A[i + k * ld], V[k + j * ld]);
-        V[i + j * ld] = inv * acc;
-      }
-      __syncthreads();
-    }
-    // H = Z L^{-H} in place, column by column: H[:, j] = (Z[:, j] - sum_{k<j} H[:, k] conj(L[j][k])) / L[j][j]
-    for (int j = 0; j < p; j++) {
-      const double inv = 1.0 / A[j + j * ld].x;
-      for (int i = tid; i < p; i += blockDim.x) {
-        cplx acc = V[i + j * ld];
-        for (int k = 0; k < j; k++) acc = acc - cmul(V[i + k * ld], conjg(A[j + k * ld]));
-        V[i + j * ld] = inv * acc;
-      }
-      __syncthreads();
-    }
+    // H = L^{-1} (D G_A D) L^{-H}: Z = L^{-1} (D G_A D) into V, then H^H = L^{-1} Z^H into T (global
+    // scratch, p x p; H Hermitian, so T = H^H is symmetrised below like H)
+    for (int i = tid; i < p; i += blockDim.x) dinv[i] = 1.0 / A[i + i * ld].x;
+    __syncthreads();
+    tri_solve_cols<false>(A, ld, dinv, p, p, [&](int m, int cc) { return (dsc[m] * dsc[cc]) * GA[m + (size_t)cc * p]; },
+                          [&](int m, int cc, cplx v) { V[m + cc * ld] = v; });
+    __syncthreads();
+    tri_solve_cols<false>(A, ld, dinv, p, p, [&](int m, int cc) { return conjg(V[cc + m * ld]); },
+                          [&](int m, int cc, cplx v) { T[m + (size_t)cc * p] = v; });
+    __syncthreads();
     // keep L (global), A <- Hermitian part of H, V <- I
     for (int e = tid; e < p * p; e += blockDim.x) {
       int i = e % p, j = e / p;
@@ -216,7 +264,7 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
       int i = e % np, j = e / np;
       cplx v = mk(0, 0);
       if (i < p && j < p) {
-        cplx a = V[i + j * ld], b = V[j + i * ld];
+        cplx a = T[i + (size_t)j * p], b = T[j + (size_t)i * p];
         v = mk(0.5 * (a.x + b.x), 0.5 * (a.y - b.y));
       }
       A[i + j * ld] = v;
@@ -298,26 +346,16 @@ __global__ void __launch_bounds__(RR_THREADS) rr_kernel(const cplx* __restrict__
   __syncthreads();
   const int nout = min(nb, r);
   if (chol) {
-    // C = D L^{-H} Q_sel: L back into A (eigenvalues are in sig), then back substitution
-    // L^H Y = Q_sel row by row from the bottom (Y into U, global, ld p)
+    // C = D L^{-H} Q_sel: L^H (upper) into A (eigenvalues are in sig), then backward substitution
+    // L^H Y = Q_sel, written scaled by D straight to C
     for (int e = tid; e < p * p; e += blockDim.x) {
       int i = e % p, j = e / p;
-      A[i + j * ld] = Lg[e];
+      A[i + j * ld] = conjg(Lg[j + (size_t)i * p]);
     }
+    for (int i = tid; i < p; i += blockDim.x) dinv[i] = 1.0 / Lg[i + (size_t)i * p].x;
     __syncthreads();
-    for (int i = p - 1; i >= 0; i--) {
-      const double inv = 1.0 / A[i + i * ld].x;
-      for (int t = tid; t < nout; t += blockDim.x) {
-        cplx acc = V[i + order[t] * rp];
-        for (int k = i + 1; k < p; k++) acc = acc - cmul(conjg(A[k + i * ld]), U[k + (size_t)t * p]);
-        U[i + (size_t)t * p] = inv * acc;
-      }
-      __syncthreads();
-    }
-    for (int e = tid; e < p * nout; e += blockDim.x) {
-      int i = e % p, t = e / p;
-      Cout[i + (size_t)t * p] = dsc[i] * U[i + (size_t)t * p];
-    }
+    tri_solve_cols<true>(A, ld, dinv, p, nout, [&](int m, int t) { return V[m + order[t] * rp]; },
+                         [&](int m, int t, cplx v) { Cout[m + (size_t)t * p] = dsc[m] * v; });
   } else {
     for (int e = tid; e < p * nout; e += blockDim.x) {
       int i = e % p, t = e / p;
