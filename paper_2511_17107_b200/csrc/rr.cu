@@ -12,8 +12,8 @@
 #include "kernels.h"
 
 constexpr int RR_MAXN = 80;
-#ifndef PC_RR_THREADS
-#define PC_RR_THREADS 1024
+#ifndef PC_RR_THREADS  // 512: a 1024-thread CTA needs a whole SM's registers and waits behind the
+#define PC_RR_THREADS 512  // other streams' kernels (C3 with 2 contexts x kbatch 4 ran at half speed)
 #endif
 constexpr int RR_THREADS = PC_RR_THREADS;
 #ifndef PC_RR_EARLY
@@ -36,9 +36,8 @@ DEV void tpair(int r, int i, int m, int& P, int& Q) {
 
 // A, V column-major with leading dimension ld (= np).  A Hermitian n x n zero-padded to np (even).
 // One round: the h = np/2 rotations (one thread each), one barrier, then the h^2 two-sided 2x2 block
-// updates of A and the np*h row updates of V as one parallel loop (<= 2 items per thread at np <= 64
-// with 1024 threads), one barrier.  Stops after a sweep without rotations, or (PC_RR_EARLY) after a
-// sweep whose largest relative off-diagonal |a_pq|^2 / |a_pp a_qq| was below max(1e-16, tol^2): cyclic
+// updates of A and the np*h row updates of V as one parallel loop, one barrier.  Stops after a sweep
+// without rotations, or (PC_RR_EARLY) after a sweep whose largest relative off-diagonal |a_pq|^2 / |a_pp a_qq| was below max(1e-16, tol^2): cyclic
 // Jacobi converges quadratically, so what that sweep leaves is O(1e-16) relative -- the sweep after it
 // would only remove rotations at the rounding level.
 DEV int jacobi_smem(cplx* A, cplx* V, int n, int np, int ld, JacSm& js, int max_sweeps, double rel_tol = 1e-16) {
