@@ -650,8 +650,12 @@ def main():
                 "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
                 "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                 "config": workload_config(W, args), "kpoints_per_rank": args.steps,
-                "parallelism": f"k-path over {world} GPU(s) from one dynamic queue, {len(ctxs)} concurrent "
-                               f"k-point solve(s) per GPU, one all-gather",
+                "parallelism": (f"k-path over {world} GPU(s) from one dynamic queue, {len(ctxs)} concurrent "
+                                f"k-point solve(s) per GPU, one all-gather"
+                                if world <= torch.cuda.device_count() else
+                                f"functional check: {world} ranks sharing {torch.cuda.device_count()} GPU(s) "
+                                f"({args.dist_backend}), one dynamic queue, {len(ctxs)} concurrent k-point solve(s) "
+                                f"per rank, one all-gather -- not a scaling result"),
                 "iters": iters, "status": status, "warmup_iters": wit, "alt_precond": alt,
                 "omega2_first_k": om[0].tolist(), "resid_max": float(rs.max()),
                 "apply": apply, "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
