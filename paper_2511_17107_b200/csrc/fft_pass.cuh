@@ -130,6 +130,9 @@ struct TileMap {
 #ifndef PC_KAG_PREFETCH
 #define PC_KAG_PREFETCH 0  // 1: last pass loads g before the DFTs (see fft_pass_kernel)
 #endif
+#ifndef PC_FFT_TWREC
+#define PC_FFT_TWREC 1  // symbol passes: step-A twiddles from two table reads and products (0: one read per k1)
+#endif
 #ifndef PC_FFT_BOUNDS
 #define PC_FFT_BOUNDS 1
 #endif
@@ -271,11 +274,37 @@ fft_pass_kernel(ColPtrs in, MutColPtrs out, ColPtrs xh, PassArgs a, int ntiles) 
 #pragma unroll
         for (int j1 = 0; j1 < R1; j1++) v[j1] = s[SI(c, j2 + R2 * j1, p)];
         Dft<R1, D>::run(v);
+        if constexpr (PC_FFT_TWREC && C == 3 && R1 % 4 == 0 && R1 >= 8) {
+          // W^{j2 k1}, k1 = 4a + b, from two table reads and <= 4 products (as xrow_step1): the
+          // per-k1 reads of the table were up to 4-way bank conflicts (lanes with different j2).
+          // Symbol passes only: under the 80-register bound of the plain passes the extra registers
+          // spill (y pass 0.98 -> 1.13 ms per 15 columns)
+          cplx w1 = tw[j2], w4 = tw[(4 * j2) % N];
+          if (D > 0) {
+            w1.y = -w1.y;
+            w4.y = -w4.y;
+          }
+          const cplx w2 = cmul(w1, w1), w3 = cmul(w2, w1);
+          cplx wa = mk(1.0, 0.0);
 #pragma unroll
-        for (int k1 = 0; k1 < R1; k1++) {
-          cplx w = tw[(j2 * k1) % N];
-          if (D > 0) w.y = -w.y;
-          s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+          for (int a4 = 0; a4 < R1 / 4; a4++) {
+            if (a4 == 1) wa = w4;
+            if (a4 > 1) wa = cmul(wa, w4);
+#pragma unroll
+            for (int b4 = 0; b4 < 4; b4++) {
+              const int k1 = 4 * a4 + b4;
+              cplx w = (b4 == 0) ? wa : (b4 == 1) ? w1 : (b4 == 2) ? w2 : w3;
+              if (a4 > 0 && b4 > 0) w = cmul(wa, w);
+              s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+            }
+          }
+        } else {
+#pragma unroll
+          for (int k1 = 0; k1 < R1; k1++) {
+            cplx w = tw[(j2 * k1) % N];
+            if (D > 0) w.y = -w.y;
+            s[SI(c, j2 + R2 * k1, p)] = (k1 == 0 || j2 == 0) ? v[k1] : cmul(v[k1], w);
+          }
         }
       }
       __syncthreads();
