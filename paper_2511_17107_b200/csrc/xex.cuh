@@ -21,18 +21,29 @@ struct XRow {
   static constexpr int P = (L % 2 == 1) ? L : L + 1;
 };
 
+// Tile shape: N <= 128: 4 output rows, 128 threads, 4 CTAs/SM; larger N: 8 rows, 256 threads, 2 CTAs/SM.
+// (At n = 128 the 4 x 128 shape was slower while the pass was shared-memory bound; after the round-2
+// shared-memory cuts it is 10 % faster, profiles/r02_experiments/xex_shape_after_cuts.txt.)  The
+// PC_XEX_TP / PC_XEX_NT / PC_XEX_MINB macros override for every N (variant builds).
 template <int N>
 struct XexCfg {
-#ifndef PC_XEX_TP
-#define PC_XEX_TP 8
-#endif
+#ifdef PC_XEX_TP
   static constexpr int TP = pow2_div(N, PC_XEX_TP);   // output rows per tile
+#else
+  static constexpr int TP = pow2_div(N, N <= 128 ? 4 : 8);
+#endif
   static constexpr int RP = TP + 2;           // rows held (1 halo row each side)
   static constexpr int P = XRow<N>::P;        // row pitch in complex
-#ifndef PC_XEX_NT
-#define PC_XEX_NT 256
-#endif
+#ifdef PC_XEX_NT
   static constexpr int NT = PC_XEX_NT;
+#else
+  static constexpr int NT = N <= 128 ? 128 : 256;
+#endif
+#ifdef PC_XEX_MINB
+  static constexpr int MINB = PC_XEX_MINB;
+#else
+  static constexpr int MINB = N <= 128 ? 4 : 2;
+#endif
   static constexpr int PPT = (N * TP + NT - 1) / NT;  // stencil points per thread
   static constexpr size_t SMEM = (size_t)3 * RP * P * sizeof(cplx) + (size_t)N * sizeof(cplx) + (size_t)RP * N;
 };
@@ -137,11 +148,8 @@ DEV void xrow_step2(const cplx* s, int npen, Store store, Row row, bool sync_inp
 #ifndef PC_XEX_COLS
 #define PC_XEX_COLS 1
 #endif
-#ifndef PC_XEX_MINB
-#define PC_XEX_MINB 2
-#endif
 template <int N, int MODE>
-__global__ void __launch_bounds__(XexCfg<N>::NT, PC_XEX_MINB)
+__global__ void __launch_bounds__(XexCfg<N>::NT, XexCfg<N>::MINB)
 xex_kernel(ColPtrs in, MutColPtrs out, const uint8_t* __restrict__ mask, EpsCoef ec, const cplx* __restrict__ twg,
            double scale, int zoff) {
   using Cfg = XexCfg<N>;
